@@ -1,0 +1,524 @@
+"""Host-side mirror of the reference's ``bsattn::`` API over the sm_100a kernels.
+
+Same names, argument meaning, layouts and error behaviour as /root/reference/proj/include/bsattn/
+(core.hpp, discovery.hpp, selection.hpp, attention.hpp), with tensors living in HBM as torch CUDA
+tensors (Z x H x L x d, bf16 or fp32).  Every compute call goes through the C ABI of
+libfpb200.so (include/fpb200.h); torch only allocates device memory and supplies the stream.
+There is no CPU fallback: a missing library or a non-CUDA tensor raises.
+
+GQA (not in the reference): K/V may carry Hkv heads with Hkv | Hq; maps and plans are
+per Q head and Q head h reads KV head h // (Hq // Hkv).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _abi
+
+# ----------------------------------------------------------------------------- errors
+# tensor.hpp:18-38
+
+
+class IoError(RuntimeError):
+    pass
+
+
+class FormatError(RuntimeError):
+    pass
+
+
+class ValidationError(RuntimeError):
+    pass
+
+
+class ConfigError(ValidationError):
+    pass
+
+
+class PlanError(ValidationError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _raise(rc: int, what: str, plan: bool = False):
+    if rc == _abi.FPB_OK:
+        return
+    msg = f"{what}: {_abi.last_error()}"
+    if rc == _abi.FPB_EVALIDATION:
+        raise (PlanError if plan else ValidationError)(msg)
+    if rc == _abi.FPB_EFORMAT:
+        raise FormatError(msg)
+    if rc == _abi.FPB_ECUDA:
+        raise CudaError(msg)
+    raise ValueError(msg)
+
+
+# ----------------------------------------------------------------------------- core.hpp
+
+kLog2e = 1.4426950408889634  # core.hpp:13
+kDefaultEpsilon = 1e-10  # core.hpp:14
+kNegSentinel = -3.4028234663852886e38  # discovery.hpp:12 (FLT_LOWEST)
+
+
+@dataclass(frozen=True)
+class BlockGrid:
+    """core.hpp:17-29."""
+
+    block_size: int
+    num_query_blocks: int
+    num_key_blocks: int
+    last_block_len: int
+
+    def block_len(self, block: int) -> int:
+        return self.last_block_len if block + 1 == self.num_key_blocks else self.block_size
+
+    def block_of(self, token: int) -> int:
+        return token // self.block_size
+
+
+def make_block_grid(seq_len: int, block_size: int) -> BlockGrid:
+    """core.hpp:31-41."""
+    if seq_len < 1:
+        raise ValidationError("sequence length must be >= 1")
+    if block_size < 1:
+        raise ValidationError("block size must be >= 1")
+    blocks = (seq_len + block_size - 1) // block_size
+    return BlockGrid(block_size, blocks, blocks, seq_len - (blocks - 1) * block_size)
+
+
+@dataclass
+class PipelineConfig:
+    """core.hpp:87-112."""
+
+    block_size: int = 128
+    alpha: float = 0.12
+    sink_tokens: int = 256
+    window_tokens: int = 512
+    scale: float = 0.0
+    epsilon: float = kDefaultEpsilon
+    rng_seed: int = 0
+
+    def validate(self) -> None:
+        if self.block_size < 1:
+            raise ConfigError("block_size must be >= 1")
+        if not (self.alpha >= 0.0):
+            raise ConfigError("alpha must be >= 0")
+        if self.window_tokens < 1:
+            raise ConfigError("window_tokens must be >= 1")
+        if not (self.epsilon > 0.0):
+            raise ConfigError("epsilon must be > 0")
+
+    def sink_blocks(self) -> int:
+        return (self.sink_tokens + self.block_size - 1) // self.block_size
+
+    def window_blocks(self) -> int:
+        return (self.window_tokens + self.block_size - 1) // self.block_size
+
+    def resolved_scale(self, head_dim: int) -> float:
+        if self.scale > 0:
+            return self.scale
+        return float(torch.tensor(1.0, dtype=torch.float32) /
+                     torch.sqrt(torch.tensor(float(head_dim), dtype=torch.float32)))
+
+
+# ----------------------------------------------------------------------------- result types
+# discovery.hpp:16-34, selection.hpp:14-38, attention.hpp:14-21
+
+
+@dataclass
+class PooledKeys:
+    data: torch.Tensor  # Z x Hkv x N x d fp32
+
+
+@dataclass
+class BlockEnergies:
+    energy: torch.Tensor
+    local_max: torch.Tensor
+
+
+@dataclass
+class BlockScoreMap:
+    energy: torch.Tensor | None
+    local_max: torch.Tensor | None
+    score: torch.Tensor
+
+
+@dataclass
+class ActiveMask:
+    active: torch.Tensor  # Z x M x N x H u8
+
+
+@dataclass
+class SparseBlockPlan:
+    indices: torch.Tensor  # Z x M x N x H i32
+    counts: torch.Tensor  # Z x M x H i32
+
+
+@dataclass
+class SelectionStats:
+    score_comparisons: int = 0
+
+
+@dataclass
+class AttentionOutput:
+    out: torch.Tensor
+    lse: torch.Tensor
+
+
+@dataclass
+class AttentionStats:
+    block_visits: int = 0
+
+
+# ----------------------------------------------------------------------------- plumbing
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return _abi.FPB_BF16
+    if t.dtype == torch.float32:
+        return _abi.FPB_F32
+    raise ValidationError(f"unsupported dtype {t.dtype} (bf16 or fp32)")
+
+
+def _dev(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValidationError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValidationError(f"{name} must be contiguous")
+    return t
+
+
+def _ptr(t: torch.Tensor | None):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(t: torch.Tensor) -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def problem(q_shape, hkv: int, config: PipelineConfig | None = None, tau: float | None = None,
+            eps: float | None = None) -> _abi.Problem:
+    Z, Hq, L, d = (int(x) for x in q_shape)
+    p = _abi.Problem()
+    _abi.lib().fpb_problem_init(C.byref(p), Z, Hq, hkv, L, d)
+    if config is not None:
+        p.block_size, p.alpha = config.block_size, config.alpha
+        p.sink_tokens, p.window_tokens = config.sink_tokens, config.window_tokens
+        p.scale, p.epsilon = config.scale, config.epsilon
+    if tau is not None:
+        p.scale = tau
+    if eps is not None:
+        p.epsilon = eps
+    return p
+
+
+_ws_cache: dict = {}
+
+
+def workspace(p: _abi.Problem, dtype_code: int, device) -> tuple[torch.Tensor | None, int]:
+    """Grow-only per-device scratch (fpb_workspace_bytes); no allocation on repeat calls."""
+    n = C.c_size_t(0)
+    _raise(_abi.lib().fpb_workspace_bytes(C.byref(p), dtype_code, C.byref(n)), "workspace")
+    if n.value == 0:
+        return None, 0
+    key = torch.device(device)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < n.value:
+        buf = torch.empty(n.value, dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf, n.value
+
+
+def _check_qk(q: torch.Tensor, k: torch.Tensor):
+    _dev(q, "queries")
+    _dev(k, "keys")
+    if q.dim() != 4 or k.dim() != 4:
+        raise ValidationError("sequence batch must be Z x H x L x d")
+    if q.dtype != k.dtype:
+        raise ValidationError("query/key dtype mismatch")
+    Z, Hq, L, d = q.shape
+    if k.shape[0] != Z or k.shape[2] != L or k.shape[3] != d or Hq % k.shape[1]:
+        raise ValidationError("query/key shape mismatch")  # core.hpp:81-85 (+ GQA)
+
+
+def make_sequence_batch(data: torch.Tensor) -> torch.Tensor:
+    """core.hpp:71-79: rejects non-4D shapes and non-finite values."""
+    if data.dim() != 4 or min(data.shape) < 1:
+        raise ValidationError("sequence batch must be Z x H x L x d")
+    if not bool(torch.isfinite(data).all()):
+        raise ValidationError("non-finite value in sequence batch")
+    return data
+
+
+# ----------------------------------------------------------------------------- discovery.hpp
+
+
+def pool_keys(keys: torch.Tensor, grid: BlockGrid) -> PooledKeys:
+    """discovery.hpp:65-70."""
+    _dev(keys, "keys")
+    Z, H, L, d = keys.shape
+    if grid.num_key_blocks * grid.block_size < L:
+        raise ValidationError("grid does not cover the key sequence")
+    p = problem((Z, H, L, d), H)
+    p.block_size = grid.block_size
+    out = torch.empty((Z, H, grid.num_key_blocks, d), dtype=torch.float32, device=keys.device)
+    _raise(_abi.lib().fpb_pool_keys(C.byref(p), _dtype_code(keys), _ptr(keys), _ptr(out),
+                                    _stream(keys)), "pool_keys")
+    return PooledKeys(out)
+
+
+def approx_block_scores(queries: torch.Tensor, pooled: PooledKeys, grid: BlockGrid,
+                        tau: float) -> BlockEnergies:
+    """discovery.hpp:75-115."""
+    _dev(queries, "queries")
+    Z, Hq, L, d = queries.shape
+    pk = _dev(pooled.data, "pooled")
+    M = grid.num_query_blocks
+    if pk.dim() != 4 or pk.shape[0] != Z or pk.shape[2] != M or pk.shape[3] != d or Hq % pk.shape[1]:
+        raise ValidationError("pooled keys shape mismatch")
+    p = problem(queries.shape, pk.shape[1], tau=tau)
+    p.block_size = grid.block_size
+    en = torch.empty((Z, Hq, M, M), dtype=torch.float32, device=queries.device)
+    lm = torch.empty_like(en)
+    ws, nws = workspace(p, _dtype_code(queries), queries.device)
+    _raise(_abi.lib().fpb_approx_block_scores(C.byref(p), _dtype_code(queries), _ptr(queries),
+                                              _ptr(pk), _ptr(en), _ptr(lm), _ptr(ws), nws,
+                                              _stream(queries)), "approx_block_scores")
+    return BlockEnergies(en, lm)
+
+
+def normalize_block_scores(energies: BlockEnergies, grid: BlockGrid,
+                           epsilon: float = kDefaultEpsilon) -> BlockScoreMap:
+    """discovery.hpp:119-148."""
+    en, lm = _dev(energies.energy, "energy"), _dev(energies.local_max, "local_max")
+    Z, H, M, _ = en.shape
+    p = problem((Z, H, (M - 1) * grid.block_size + grid.last_block_len, 128), H, eps=epsilon)
+    p.block_size = grid.block_size
+    score = torch.empty_like(en)
+    _raise(_abi.lib().fpb_normalize_block_scores(C.byref(p), _ptr(en), _ptr(lm), _ptr(score),
+                                                 _stream(en)), "normalize_block_scores")
+    return BlockScoreMap(en, lm, score)
+
+
+def discover(queries: torch.Tensor, keys: torch.Tensor, grid: BlockGrid, tau: float,
+             epsilon: float = kDefaultEpsilon, maps: bool = True) -> BlockScoreMap:
+    """discovery.hpp:153-159 (pool + fused approximation + normalisation in two launches).
+
+    maps=False skips materialising energy/local_max (score only)."""
+    _check_qk(queries, keys)
+    Z, Hq, L, d = queries.shape
+    M = grid.num_query_blocks
+    p = problem(queries.shape, keys.shape[1], tau=tau, eps=epsilon)
+    p.block_size = grid.block_size
+    dev = queries.device
+    score = torch.empty((Z, Hq, M, M), dtype=torch.float32, device=dev)
+    en = torch.empty_like(score) if maps else None
+    lm = torch.empty_like(score) if maps else None
+    ws, nws = workspace(p, _dtype_code(queries), dev)
+    _raise(_abi.lib().fpb_discover(C.byref(p), _dtype_code(queries), _ptr(queries), _ptr(keys),
+                                   _ptr(en), _ptr(lm), _ptr(score), _ptr(ws), nws,
+                                   _stream(queries)), "discover")
+    return BlockScoreMap(en, lm, score)
+
+
+# ----------------------------------------------------------------------------- selection.hpp
+
+
+def max_threshold_mask(scores, config: PipelineConfig,
+                       stats: SelectionStats | None = None) -> ActiveMask:
+    """selection.hpp:63-92 (and the BlockScoreMap overload, :161-164)."""
+    config.validate()
+    score = scores.score if isinstance(scores, BlockScoreMap) else scores
+    _dev(score, "score")
+    if score.dim() != 4:
+        raise ValidationError("score map must be Z x H x M x N")
+    Z, H, M, N = score.shape
+    if M != N:
+        raise ValidationError("score map must be square (M == N)")
+    p = problem((Z, H, (M - 1) * config.block_size + 1, 128), H, config=config)
+    mask = torch.empty((Z, M, N, H), dtype=torch.uint8, device=score.device)
+    cmp = torch.zeros(1, dtype=torch.int64, device=score.device) if stats is not None else None
+    _raise(_abi.lib().fpb_max_threshold_mask(C.byref(p), _ptr(score), _ptr(mask), _ptr(cmp),
+                                             _stream(score)), "max_threshold_mask")
+    if stats is not None:
+        stats.score_comparisons += int(cmp.item())
+    return ActiveMask(mask)
+
+
+def compress_indices(mask: ActiveMask) -> SparseBlockPlan:
+    """selection.hpp:176-192."""
+    m = _dev(mask.active, "mask")
+    Z, M, N, H = m.shape
+    p = problem((Z, H, (M - 1) * 128 + 1, 128), H)
+    idx = torch.empty((Z, M, N, H), dtype=torch.int32, device=m.device)
+    counts = torch.empty((Z, M, H), dtype=torch.int32, device=m.device)
+    _raise(_abi.lib().fpb_compress_indices(C.byref(p), _ptr(m), _ptr(idx), _ptr(counts),
+                                           _stream(m)), "compress_indices")
+    return SparseBlockPlan(idx, counts)
+
+
+def visit_count(plan: SparseBlockPlan) -> int:
+    """selection.hpp:195-200."""
+    c = _dev(plan.counts, "counts")
+    Z, M, H = c.shape
+    p = problem((Z, H, (M - 1) * 128 + 1, 128), H)
+    total = torch.zeros(1, dtype=torch.int64, device=c.device)
+    _raise(_abi.lib().fpb_visit_count(C.byref(p), _ptr(c), _ptr(total), _stream(c)), "visit_count")
+    return int(total.item())
+
+
+def density(plan: SparseBlockPlan, grid: BlockGrid) -> float:
+    """selection.hpp:203-209."""
+    Z, _, H = plan.counts.shape
+    M = grid.num_query_blocks
+    return visit_count(plan) / (Z * H * (M * (M + 1) / 2.0))
+
+
+def discover_select(queries: torch.Tensor, keys: torch.Tensor, config: PipelineConfig,
+                    want_score: bool = False, want_mask: bool = False,
+                    want_energy: bool = False):
+    """Fused discover -> max_threshold_mask -> compress_indices (one pass over Q).
+
+    Returns (SparseBlockPlan, BlockScoreMap | None, ActiveMask | None)."""
+    config.validate()
+    _check_qk(queries, keys)
+    Z, Hq, L, d = queries.shape
+    grid = make_block_grid(L, config.block_size)
+    M = grid.num_query_blocks
+    dev = queries.device
+    p = problem(queries.shape, keys.shape[1], config=config)
+    idx = torch.empty((Z, M, M, Hq), dtype=torch.int32, device=dev)
+    counts = torch.empty((Z, M, Hq), dtype=torch.int32, device=dev)
+    score = torch.empty((Z, Hq, M, M), dtype=torch.float32, device=dev) if want_score else None
+    en = torch.empty((Z, Hq, M, M), dtype=torch.float32, device=dev) if want_energy else None
+    lm = torch.empty_like(en) if want_energy else None
+    mask = torch.empty((Z, M, M, Hq), dtype=torch.uint8, device=dev) if want_mask else None
+    ws, nws = workspace(p, _dtype_code(queries), dev)
+    _raise(_abi.lib().fpb_discover_select(C.byref(p), _dtype_code(queries), _ptr(queries),
+                                          _ptr(keys), _ptr(en), _ptr(lm), _ptr(score), _ptr(mask),
+                                          _ptr(idx), _ptr(counts), _ptr(ws), nws,
+                                          _stream(queries)), "discover_select")
+    smap = BlockScoreMap(en, lm, score) if want_score else None
+    return SparseBlockPlan(idx, counts), smap, (ActiveMask(mask) if want_mask else None)
+
+
+# ----------------------------------------------------------------------------- attention.hpp
+
+
+def _check_qkv(q, k, v):
+    _check_qk(q, k)
+    _dev(v, "values")
+    if v.shape != k.shape or v.dtype != k.dtype:
+        raise ValidationError("key/value shape mismatch")
+
+
+def _out_code(out_dtype, q):
+    out_dtype = out_dtype or q.dtype
+    return out_dtype, (_abi.FPB_BF16 if out_dtype == torch.bfloat16 else _abi.FPB_F32)
+
+
+def block_sparse_attention(queries, keys, values, plan: SparseBlockPlan, grid: BlockGrid,
+                           tau: float, stats: AttentionStats | None = None,
+                           out_dtype: torch.dtype | None = None) -> AttentionOutput:
+    """attention.hpp:38-132.  Raises PlanError for a block index outside [0, N)."""
+    _check_qkv(queries, keys, values)
+    Z, Hq, L, d = queries.shape
+    M = grid.num_query_blocks
+    idx, counts = _dev(plan.indices, "indices"), _dev(plan.counts, "counts")
+    if tuple(idx.shape) != (Z, M, M, Hq) or tuple(counts.shape) != (Z, M, Hq):
+        raise ValidationError("plan shape does not match grid/batch")
+    p = problem(queries.shape, keys.shape[1], tau=tau)
+    p.block_size = grid.block_size
+    dev = queries.device
+    out_dtype, oc = _out_code(out_dtype, queries)
+    out = torch.empty(queries.shape, dtype=out_dtype, device=dev)
+    lse = torch.empty((Z, Hq, L), dtype=torch.float32, device=dev)
+    aux = torch.zeros(2, dtype=torch.int64, device=dev)  # [visits, plan_error]
+    ws, nws = workspace(p, _dtype_code(queries), dev)
+    _raise(_abi.lib().fpb_block_sparse_attention(
+        C.byref(p), _dtype_code(queries), _ptr(queries), _ptr(keys), _ptr(values), _ptr(idx),
+        _ptr(counts), oc, _ptr(out), _ptr(lse), C.c_void_p(aux.data_ptr()),
+        C.c_void_p(aux.data_ptr() + 8), _ptr(ws), nws, _stream(queries)),
+        "block_sparse_attention")
+    visits, err = (int(x) for x in aux.tolist())
+    if err:
+        raise PlanError(f"plan row lists a block index outside [0, {M})")
+    if stats is not None:
+        stats.block_visits += visits
+    return AttentionOutput(out, lse)
+
+
+def dense_attention(queries, keys, values, tau: float,
+                    out_dtype: torch.dtype | None = None) -> AttentionOutput:
+    """attention.hpp:135-174 — the dense causal kernel (speedup denominator)."""
+    _check_qkv(queries, keys, values)
+    Z, Hq, L, d = queries.shape
+    p = problem(queries.shape, keys.shape[1], tau=tau)
+    dev = queries.device
+    out_dtype, oc = _out_code(out_dtype, queries)
+    out = torch.empty(queries.shape, dtype=out_dtype, device=dev)
+    lse = torch.empty((Z, Hq, L), dtype=torch.float32, device=dev)
+    ws, nws = workspace(p, _dtype_code(queries), dev)
+    _raise(_abi.lib().fpb_dense_attention(C.byref(p), _dtype_code(queries), _ptr(queries),
+                                          _ptr(keys), _ptr(values), oc, _ptr(out), _ptr(lse),
+                                          _ptr(ws), nws, _stream(queries)), "dense_attention")
+    return AttentionOutput(out, lse)
+
+
+def full_causal_plan(batch: int, heads: int, grid: BlockGrid, device="cuda") -> SparseBlockPlan:
+    """attention.hpp:178-192."""
+    M = grid.num_query_blocks
+    p = problem((batch, heads, (M - 1) * grid.block_size + 1, 128), heads)
+    idx = torch.empty((batch, M, M, heads), dtype=torch.int32, device=device)
+    counts = torch.empty((batch, M, heads), dtype=torch.int32, device=device)
+    _raise(_abi.lib().fpb_full_causal_plan(C.byref(p), _ptr(idx), _ptr(counts),
+                                           C.c_void_p(torch.cuda.current_stream(device).cuda_stream)),
+           "full_causal_plan")
+    return SparseBlockPlan(idx, counts)
+
+
+def prefill(queries, keys, values, config: PipelineConfig,
+            out_dtype: torch.dtype | None = None, stats: AttentionStats | None = None):
+    """The whole FlashPrefill step (acceptance.cpp:357-360) on device tensors:
+    fused discover+select, then block-sparse attention.  Returns (AttentionOutput, plan)."""
+    plan, _, _ = discover_select(queries, keys, config)
+    grid = make_block_grid(queries.shape[2], config.block_size)
+    tau = config.resolved_scale(queries.shape[3])
+    return block_sparse_attention(queries, keys, values, plan, grid, tau, stats, out_dtype), plan
+
+
+def prefill_host(q_host, k_host, v_host, config: PipelineConfig, out_host, lse_host,
+                 idx_host=None, counts_host=None) -> int:
+    """fpb_host_prefill over HOST tensors (pinned recommended): H2D, kernels, D2H, sync.
+
+    Returns block visits.  This is the reference-facing end-to-end call bench.py times."""
+    for t in (q_host, k_host, v_host, out_host, lse_host):
+        if t.is_cuda or not t.is_contiguous():
+            raise ValidationError("prefill_host takes contiguous host tensors")
+    p = problem(q_host.shape, k_host.shape[1], config=config)
+    vis = C.c_uint64(0)
+    oc = _abi.FPB_BF16 if out_host.dtype == torch.bfloat16 else _abi.FPB_F32
+    _raise(_abi.lib().fpb_host_prefill(C.byref(p), _dtype_code(q_host), _ptr(q_host),
+                                       _ptr(k_host), _ptr(v_host), oc, _ptr(out_host),
+                                       _ptr(lse_host), _ptr(idx_host), _ptr(counts_host),
+                                       C.byref(vis)), "prefill_host")
+    return vis.value
+
+
+def flops_dense_causal(Z: int, Hq: int, L: int, d: int) -> float:
+    """Dense-causal-equivalent attention FLOPs: 4 d Z Hq L(L+1)/2."""
+    return 4.0 * d * Z * Hq * L * (L + 1) / 2.0
+
+
+def flops_sparse(visits_off_diag: int, visits_diag: int, d: int = 128, B: int = 128) -> float:
+    """Algorithmic FLOPs of the visited blocks: 4 d B^2 per off-diagonal visit, 4 d B(B+1)/2 per
+    diagonal visit."""
+    return 4.0 * d * (visits_off_diag * B * B + visits_diag * B * (B + 1) / 2.0)
+

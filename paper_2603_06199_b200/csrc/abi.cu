@@ -1,0 +1,607 @@
+// abi.cu — the C ABI (include/fpb200.h): validation, workspace carving, tensor maps, launches,
+// and the host-buffer entry points the C++ drop-in layer uses.
+//
+// Validation mirrors the reference's exceptions (return code 2 == ValidationError / ConfigError /
+// PlanError):  PipelineConfig::validate (core.hpp:96-101), make_block_grid (core.hpp:31-41),
+// require_same_shape / require_qkv (core.hpp:81-85, attention.hpp:25-30), plan shape
+// (attention.hpp:47-49) and the per-visit block range check (attention.hpp:78-81).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/fpb200.h"
+#include "fp_kernels.h"
+
+namespace fpb {
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(FPB_ECUDA, "%s: CUDA error %d (%s)", where, (int)e, cudaGetErrorString(e));
+}
+
+#define FPB_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
+  } while (0)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+size_t align_up(size_t x, size_t a = 1024) { return (x + a - 1) / a * a; }
+
+// Resolves the problem into kernel dims; returns 0 or an error code.
+int resolve(const fpb_problem* p, Dims* D) {
+  if (!p) return fail(FPB_EUSAGE, "null problem");
+  if (p->Z < 1 || p->Hq < 1 || p->Hkv < 1 || p->L < 1 || p->d < 1)
+    return fail(FPB_EVALIDATION, "sequence batch dims must be >= 1");
+  if (p->Hq % p->Hkv) return fail(FPB_EVALIDATION, "Hq must be a multiple of Hkv");
+  if (p->block_size < 1) return fail(FPB_EVALIDATION, "block_size must be >= 1");
+  if (!(p->alpha >= 0.0f)) return fail(FPB_EVALIDATION, "alpha must be >= 0");
+  if (p->window_tokens < 1) return fail(FPB_EVALIDATION, "window_tokens must be >= 1");
+  if (p->sink_tokens < 0) return fail(FPB_EVALIDATION, "sink_tokens must be >= 0");
+  if (!(p->epsilon > 0.0f)) return fail(FPB_EVALIDATION, "epsilon must be > 0");
+  if (p->d != kHeadDim) return fail(FPB_EVALIDATION, "head_dim %lld unsupported (must be 128)", (long long)p->d);
+  if (p->block_size != kBlock)
+    return fail(FPB_EVALIDATION, "block_size %d unsupported (must be 128)", p->block_size);
+  if (p->L > (int64_t)1 << 30 || p->Z * p->Hq > (int64_t)1 << 24)
+    return fail(FPB_EVALIDATION, "problem too large");
+  D->Z = (int)p->Z;
+  D->Hq = (int)p->Hq;
+  D->Hkv = (int)p->Hkv;
+  D->L = (int)p->L;
+  D->M = (int)((p->L + kBlock - 1) / kBlock);
+  D->group = D->Hq / D->Hkv;
+  D->last_len = (int)(p->L - (int64_t)(D->M - 1) * kBlock);
+  const float tau = p->scale > 0.0f ? p->scale : 1.0f / sqrtf((float)p->d);  // core.hpp:109-111
+  D->to_bits = tau * kLog2e;
+  D->eps = p->epsilon;
+  D->alpha = p->alpha;
+  D->sink_blocks = (p->sink_tokens + kBlock - 1) / kBlock;      // core.hpp:103-105
+  D->window_blocks = (p->window_tokens + kBlock - 1) / kBlock;  // core.hpp:106-108
+  return FPB_OK;
+}
+
+int check_dtype(fpb_dtype t) {
+  return (t == FPB_F32 || t == FPB_BF16) ? FPB_OK : fail(FPB_EUSAGE, "bad dtype %d", (int)t);
+}
+
+size_t q_elems(const Dims& D) { return (size_t)D.Z * D.Hq * D.L * kHeadDim; }
+size_t kv_elems(const Dims& D) { return (size_t)D.Z * D.Hkv * D.L * kHeadDim; }
+size_t map_elems(const Dims& D) { return (size_t)D.Z * D.Hq * D.M * D.M; }
+size_t kbar_split_bytes(const Dims& D) { return 2ull * D.Z * D.Hkv * D.M * kHeadDim * 2; }
+
+// Workspace layouts.  discover: [kbar split][Q hi/lo planes if fp32]
+//                     attention: [Q bf16][K bf16][V bf16] if fp32
+size_t ws_discover(const Dims& D, fpb_dtype t) {
+  size_t b = align_up(kbar_split_bytes(D));
+  if (t == FPB_F32) b += align_up(2 * q_elems(D) * 2);
+  return b;
+}
+size_t ws_attention(const Dims& D, fpb_dtype t) {
+  return t == FPB_F32 ? align_up(q_elems(D) * 2) + 2 * align_up(kv_elems(D) * 2) : 0;
+}
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int need_ws(size_t have, size_t need, void* ws) {
+  if (need && (!ws || have < need))
+    return fail(FPB_EUSAGE, "workspace too small: need %zu bytes, have %zu", need, have);
+  return FPB_OK;
+}
+
+// Discovery front half: pool k̄ (+split) and stage Q planes; returns the Q plane pointer.
+int discover_prepare(const Dims& D, fpb_dtype t, const void* Q, const void* K, float* pooled,
+                     void* ws, cudaStream_t st, __nv_bfloat16** kbar_split,
+                     const __nv_bfloat16** q_planes) {
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  *kbar_split = reinterpret_cast<__nv_bfloat16*>(w);
+  FPB_CUDA(launch_pool_keys(D, t == FPB_BF16, K, pooled, *kbar_split, st));
+  if (t == FPB_BF16) {
+    *q_planes = static_cast<const __nv_bfloat16*>(Q);
+  } else {
+    __nv_bfloat16* qp = reinterpret_cast<__nv_bfloat16*>(w + align_up(kbar_split_bytes(D)));
+    FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(Q), qp, qp + q_elems(D), q_elems(D), st));
+    *q_planes = qp;
+  }
+  return FPB_OK;
+}
+
+}  // namespace
+
+bool make_tmap_rows128(CUtensorMap* map, const void* base, uint64_t rows, uint64_t planes) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)kHeadDim, rows, planes};
+  cuuint64_t strides[2] = {(cuuint64_t)kHeadDim * 2, rows * kHeadDim * 2};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace fpb
+
+using namespace fpb;
+
+extern "C" {
+
+void fpb_problem_init(fpb_problem* p, int64_t Z, int64_t Hq, int64_t Hkv, int64_t L, int64_t d) {
+  p->Z = Z;
+  p->Hq = Hq;
+  p->Hkv = Hkv;
+  p->L = L;
+  p->d = d;
+  p->block_size = 128;
+  p->alpha = 0.12f;
+  p->sink_tokens = 256;
+  p->window_tokens = 512;
+  p->scale = 0.0f;
+  p->epsilon = 1e-10f;
+}
+
+int fpb_version(void) { return 1; }
+
+const char* fpb_last_error(void) { return g_err.c_str(); }
+
+int fpb_workspace_bytes(const fpb_problem* p, fpb_dtype dtype, size_t* bytes) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc || (rc = check_dtype(dtype))) return rc;
+  if (!bytes) return fail(FPB_EUSAGE, "null bytes");
+  const size_t a = ws_discover(D, dtype), b = ws_attention(D, dtype);
+  *bytes = a > b ? a : b;
+  return FPB_OK;
+}
+
+int fpb_pool_keys(const fpb_problem* p, fpb_dtype dtype, const void* K, float* pooled,
+                  void* stream) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc || (rc = check_dtype(dtype))) return rc;
+  if (!K || !pooled) return fail(FPB_EUSAGE, "null pointer");
+  FPB_CUDA(launch_pool_keys(D, dtype == FPB_BF16, K, pooled, nullptr, S(stream)));
+  return FPB_OK;
+}
+
+int fpb_approx_block_scores(const fpb_problem* p, fpb_dtype dtype, const void* Q,
+                            const float* pooled, float* energy, float* local_max, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc || (rc = check_dtype(dtype))) return rc;
+  if (!Q || !pooled || !energy || !local_max) return fail(FPB_EUSAGE, "null pointer");
+  if ((rc = need_ws(workspace_bytes, ws_discover(D, dtype), workspace))) return rc;
+  uint8_t* w = static_cast<uint8_t*>(workspace);
+  __nv_bfloat16* kbar = reinterpret_cast<__nv_bfloat16*>(w);
+  FPB_CUDA(launch_split_pooled(D, pooled, kbar, S(stream)));
+  const __nv_bfloat16* qp = static_cast<const __nv_bfloat16*>(Q);
+  if (dtype == FPB_F32) {
+    __nv_bfloat16* q2 = reinterpret_cast<__nv_bfloat16*>(w + align_up(kbar_split_bytes(D)));
+    FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(Q), q2, q2 + q_elems(D), q_elems(D),
+                                S(stream)));
+    qp = q2;
+  }
+  DiscoverOut o;
+  o.energy = energy;
+  o.local_max = local_max;
+  o.normalize = false;
+  FPB_CUDA(launch_discover(D, dtype == FPB_F32 ? 2 : 1, qp, kbar, o, S(stream)));
+  return FPB_OK;
+}
+
+int fpb_normalize_block_scores(const fpb_problem* p, const float* energy, const float* local_max,
+                               float* score, void* stream) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc) return rc;
+  if (!energy || !local_max || !score) return fail(FPB_EUSAGE, "null pointer");
+  FPB_CUDA(launch_normalize(D, energy, local_max, score, S(stream)));
+  return FPB_OK;
+}
+
+int fpb_discover_select(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                        float* energy, float* local_max, float* score, uint8_t* mask, int32_t* idx,
+                        int32_t* counts, void* workspace, size_t workspace_bytes, void* stream) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc || (rc = check_dtype(dtype))) return rc;
+  if (!Q || !K) return fail(FPB_EUSAGE, "null pointer");
+  if ((idx == nullptr) != (counts == nullptr))
+    return fail(FPB_EUSAGE, "idx and counts must be given together");
+  if ((rc = need_ws(workspace_bytes, ws_discover(D, dtype), workspace))) return rc;
+  __nv_bfloat16* kbar;
+  const __nv_bfloat16* qp;
+  if ((rc = discover_prepare(D, dtype, Q, K, nullptr, workspace, S(stream), &kbar, &qp))) return rc;
+  DiscoverOut o;
+  o.energy = energy;
+  o.local_max = local_max;
+  o.score = score;
+  o.mask = mask;
+  o.idx = idx;
+  o.counts = counts;
+  FPB_CUDA(launch_discover(D, dtype == FPB_F32 ? 2 : 1, qp, kbar, o, S(stream)));
+  return FPB_OK;
+}
+
+int fpb_discover(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                 float* energy, float* local_max, float* score, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+  if (!score) return fail(FPB_EUSAGE, "null score");
+  return fpb_discover_select(p, dtype, Q, K, energy, local_max, score, nullptr, nullptr, nullptr,
+                             workspace, workspace_bytes, stream);
+}
+
+int fpb_max_threshold_mask(const fpb_problem* p, const float* score, uint8_t* mask,
+                           unsigned long long* comparisons, void* stream) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc) return rc;
+  if (!score || !mask) return fail(FPB_EUSAGE, "null pointer");
+  FPB_CUDA(launch_threshold(D, score, mask, comparisons, S(stream)));
+  return FPB_OK;
+}
+
+int fpb_compress_indices(const fpb_problem* p, const uint8_t* mask, int32_t* idx, int32_t* counts,
+                         void* stream) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc) return rc;
+  if (!mask || !idx || !counts) return fail(FPB_EUSAGE, "null pointer");
+  FPB_CUDA(launch_compress(D, mask, idx, counts, S(stream)));
+  return FPB_OK;
+}
+
+int fpb_visit_count(const fpb_problem* p, const int32_t* counts, unsigned long long* total,
+                    void* stream) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc) return rc;
+  if (!counts || !total) return fail(FPB_EUSAGE, "null pointer");
+  FPB_CUDA(launch_visit_count(D, counts, total, S(stream)));
+  return FPB_OK;
+}
+
+int fpb_full_causal_plan(const fpb_problem* p, int32_t* idx, int32_t* counts, void* stream) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc) return rc;
+  if (!idx || !counts) return fail(FPB_EUSAGE, "null pointer");
+  FPB_CUDA(launch_full_causal_plan(D, idx, counts, S(stream)));
+  return FPB_OK;
+}
+
+}  // extern "C"
+
+static int attention_common(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                            const void* V, const int32_t* idx, const int32_t* counts,
+                            fpb_dtype out_dtype, void* out, float* lse,
+                            unsigned long long* visits, int32_t* plan_error, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc || (rc = check_dtype(dtype)) || (rc = check_dtype(out_dtype))) return rc;
+  if (!Q || !K || !V || !out || !lse) return fail(FPB_EUSAGE, "null pointer");
+  if ((rc = need_ws(workspace_bytes, ws_attention(D, dtype), workspace))) return rc;
+  const __nv_bfloat16 *q = static_cast<const __nv_bfloat16*>(Q),
+                      *k = static_cast<const __nv_bfloat16*>(K),
+                      *v = static_cast<const __nv_bfloat16*>(V);
+  if (dtype == FPB_F32) {
+    uint8_t* w = static_cast<uint8_t*>(workspace);
+    __nv_bfloat16* q2 = reinterpret_cast<__nv_bfloat16*>(w);
+    __nv_bfloat16* k2 = reinterpret_cast<__nv_bfloat16*>(w + align_up(q_elems(D) * 2));
+    __nv_bfloat16* v2 = reinterpret_cast<__nv_bfloat16*>(w + align_up(q_elems(D) * 2) +
+                                                         align_up(kv_elems(D) * 2));
+    FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(Q), q2, nullptr, q_elems(D), S(stream)));
+    FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(K), k2, nullptr, kv_elems(D), S(stream)));
+    FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(V), v2, nullptr, kv_elems(D), S(stream)));
+    q = q2;
+    k = k2;
+    v = v2;
+  }
+  FPB_CUDA(launch_attention(D, q, k, v, idx, counts, out_dtype == FPB_BF16, out, lse, visits,
+                            plan_error, S(stream)));
+  return FPB_OK;
+}
+
+extern "C" {
+
+int fpb_block_sparse_attention(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                               const void* V, const int32_t* idx, const int32_t* counts,
+                               fpb_dtype out_dtype, void* out, float* lse,
+                               unsigned long long* visits, int32_t* plan_error, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  if (!idx || !counts) return fail(FPB_EUSAGE, "null plan");
+  return attention_common(p, dtype, Q, K, V, idx, counts, out_dtype, out, lse, visits, plan_error,
+                          workspace, workspace_bytes, stream);
+}
+
+int fpb_dense_attention(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                        const void* V, fpb_dtype out_dtype, void* out, float* lse, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+  return attention_common(p, dtype, Q, K, V, nullptr, nullptr, out_dtype, out, lse, nullptr,
+                          nullptr, workspace, workspace_bytes, stream);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ host-buffer entry points
+namespace {
+
+// Grow-only per-thread device arena for the host entry points (no allocation on repeat calls).
+struct Arena {
+  void* ptr = nullptr;
+  size_t cap = 0;
+  cudaStream_t stream = nullptr;
+  ~Arena() {
+    if (ptr) cudaFree(ptr);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+thread_local Arena g_arena;
+
+int arena_get(size_t bytes, uint8_t** out, cudaStream_t* st) {
+  if (!g_arena.stream) FPB_CUDA(cudaStreamCreateWithFlags(&g_arena.stream, cudaStreamNonBlocking));
+  if (bytes > g_arena.cap) {
+    if (g_arena.ptr) FPB_CUDA(cudaFree(g_arena.ptr));
+    g_arena.ptr = nullptr;
+    g_arena.cap = 0;
+    FPB_CUDA(cudaMalloc(&g_arena.ptr, bytes));
+    g_arena.cap = bytes;
+  }
+  *out = static_cast<uint8_t*>(g_arena.ptr);
+  *st = g_arena.stream;
+  return FPB_OK;
+}
+
+struct Carve {
+  uint8_t* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t bytes) {
+    T* p = reinterpret_cast<T*>(base + off);
+    off += align_up(bytes ? bytes : 1);
+    return p;
+  }
+};
+
+size_t dsz(fpb_dtype t) { return t == FPB_F32 ? 4 : 2; }
+
+}  // namespace
+
+extern "C" {
+
+int fpb_host_discover(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                      float* energy, float* local_max, float* score) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc || (rc = check_dtype(dtype))) return rc;
+  if (!Q || !K || !score) return fail(FPB_EUSAGE, "null pointer");
+  const size_t qb = q_elems(D) * dsz(dtype), kb = kv_elems(D) * dsz(dtype),
+               mb = map_elems(D) * 4, wsb = ws_discover(D, dtype);
+  const size_t need = align_up(qb) + align_up(kb) + 3 * align_up(mb) + align_up(wsb);
+  uint8_t* base;
+  cudaStream_t st;
+  if ((rc = arena_get(need, &base, &st))) return rc;
+  Carve c{base};
+  void* dq = c.take<void>(qb);
+  void* dk = c.take<void>(kb);
+  float* de = c.take<float>(mb);
+  float* dl = c.take<float>(mb);
+  float* ds = c.take<float>(mb);
+  void* ws = c.take<void>(wsb);
+  FPB_CUDA(cudaMemcpyAsync(dq, Q, qb, cudaMemcpyHostToDevice, st));
+  FPB_CUDA(cudaMemcpyAsync(dk, K, kb, cudaMemcpyHostToDevice, st));
+  if ((rc = fpb_discover(p, dtype, dq, dk, energy ? de : nullptr, local_max ? dl : nullptr, ds, ws,
+                         wsb, st)))
+    return rc;
+  if (energy) FPB_CUDA(cudaMemcpyAsync(energy, de, mb, cudaMemcpyDeviceToHost, st));
+  if (local_max) FPB_CUDA(cudaMemcpyAsync(local_max, dl, mb, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaMemcpyAsync(score, ds, mb, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaStreamSynchronize(st));
+  return FPB_OK;
+}
+
+int fpb_host_max_threshold_mask(const fpb_problem* p, const float* score, uint8_t* mask,
+                                unsigned long long* comparisons) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc) return rc;
+  if (!score || !mask) return fail(FPB_EUSAGE, "null pointer");
+  const size_t sb = map_elems(D) * 4, mb = map_elems(D);
+  uint8_t* base;
+  cudaStream_t st;
+  if ((rc = arena_get(align_up(sb) + align_up(mb) + 1024, &base, &st))) return rc;
+  Carve c{base};
+  float* ds = c.take<float>(sb);
+  uint8_t* dm = c.take<uint8_t>(mb);
+  unsigned long long* dc = c.take<unsigned long long>(8);
+  FPB_CUDA(cudaMemcpyAsync(ds, score, sb, cudaMemcpyHostToDevice, st));
+  FPB_CUDA(cudaMemsetAsync(dc, 0, 8, st));
+  if ((rc = fpb_max_threshold_mask(p, ds, dm, dc, st))) return rc;
+  FPB_CUDA(cudaMemcpyAsync(mask, dm, mb, cudaMemcpyDeviceToHost, st));
+  unsigned long long cmp = 0;
+  FPB_CUDA(cudaMemcpyAsync(&cmp, dc, 8, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaStreamSynchronize(st));
+  if (comparisons) *comparisons += cmp;
+  return FPB_OK;
+}
+
+int fpb_host_compress_indices(const fpb_problem* p, const uint8_t* mask, int32_t* idx,
+                              int32_t* counts) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc) return rc;
+  if (!mask || !idx || !counts) return fail(FPB_EUSAGE, "null pointer");
+  const size_t mb = map_elems(D), ib = map_elems(D) * 4, cb = (size_t)D.Z * D.M * D.Hq * 4;
+  uint8_t* base;
+  cudaStream_t st;
+  if ((rc = arena_get(align_up(mb) + align_up(ib) + align_up(cb), &base, &st))) return rc;
+  Carve c{base};
+  uint8_t* dm = c.take<uint8_t>(mb);
+  int32_t* di = c.take<int32_t>(ib);
+  int32_t* dc = c.take<int32_t>(cb);
+  FPB_CUDA(cudaMemcpyAsync(dm, mask, mb, cudaMemcpyHostToDevice, st));
+  if ((rc = fpb_compress_indices(p, dm, di, dc, st))) return rc;
+  FPB_CUDA(cudaMemcpyAsync(idx, di, ib, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaMemcpyAsync(counts, dc, cb, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaStreamSynchronize(st));
+  return FPB_OK;
+}
+
+}  // extern "C"
+
+static int host_attention(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                          const void* V, const int32_t* idx, const int32_t* counts,
+                          fpb_dtype out_dtype, void* out, float* lse,
+                          unsigned long long* visits) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc || (rc = check_dtype(dtype)) || (rc = check_dtype(out_dtype))) return rc;
+  if (!Q || !K || !V || !out || !lse) return fail(FPB_EUSAGE, "null pointer");
+  const size_t qb = q_elems(D) * dsz(dtype), kb = kv_elems(D) * dsz(dtype),
+               ob = q_elems(D) * dsz(out_dtype), lb = (size_t)D.Z * D.Hq * D.L * 4,
+               ib = idx ? map_elems(D) * 4 : 0, cb = idx ? (size_t)D.Z * D.M * D.Hq * 4 : 0,
+               wsb = ws_attention(D, dtype);
+  const size_t need = align_up(qb) + 2 * align_up(kb) + align_up(ob) + align_up(lb) +
+                      align_up(ib) + align_up(cb) + align_up(wsb) + 2048;
+  uint8_t* base;
+  cudaStream_t st;
+  if ((rc = arena_get(need, &base, &st))) return rc;
+  Carve c{base};
+  void* dq = c.take<void>(qb);
+  void* dk = c.take<void>(kb);
+  void* dv = c.take<void>(kb);
+  void* dout = c.take<void>(ob);
+  float* dl = c.take<float>(lb);
+  int32_t* di = c.take<int32_t>(ib);
+  int32_t* dc = c.take<int32_t>(cb);
+  unsigned long long* dvis = c.take<unsigned long long>(8);
+  int32_t* derr = c.take<int32_t>(4);
+  void* ws = c.take<void>(wsb);
+  FPB_CUDA(cudaMemcpyAsync(dq, Q, qb, cudaMemcpyHostToDevice, st));
+  FPB_CUDA(cudaMemcpyAsync(dk, K, kb, cudaMemcpyHostToDevice, st));
+  FPB_CUDA(cudaMemcpyAsync(dv, V, kb, cudaMemcpyHostToDevice, st));
+  FPB_CUDA(cudaMemsetAsync(dvis, 0, 8, st));
+  FPB_CUDA(cudaMemsetAsync(derr, 0, 4, st));
+  if (idx) {
+    FPB_CUDA(cudaMemcpyAsync(di, idx, ib, cudaMemcpyHostToDevice, st));
+    FPB_CUDA(cudaMemcpyAsync(dc, counts, cb, cudaMemcpyHostToDevice, st));
+    rc = fpb_block_sparse_attention(p, dtype, dq, dk, dv, di, dc, out_dtype, dout, dl, dvis, derr,
+                                    ws, wsb, st);
+  } else {
+    rc = fpb_dense_attention(p, dtype, dq, dk, dv, out_dtype, dout, dl, ws, wsb, st);
+  }
+  if (rc) return rc;
+  FPB_CUDA(cudaMemcpyAsync(out, dout, ob, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaMemcpyAsync(lse, dl, lb, cudaMemcpyDeviceToHost, st));
+  unsigned long long vis = 0;
+  int32_t err = 0;
+  FPB_CUDA(cudaMemcpyAsync(&vis, dvis, 8, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaMemcpyAsync(&err, derr, 4, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaStreamSynchronize(st));
+  if (err) return fail(FPB_EVALIDATION, "plan row lists a block index outside [0, %d)", D.M);
+  if (visits) *visits += vis;
+  return FPB_OK;
+}
+
+extern "C" {
+
+int fpb_host_block_sparse_attention(const fpb_problem* p, fpb_dtype dtype, const void* Q,
+                                    const void* K, const void* V, const int32_t* idx,
+                                    const int32_t* counts, fpb_dtype out_dtype, void* out,
+                                    float* lse, unsigned long long* visits) {
+  if (!idx || !counts) return fail(FPB_EUSAGE, "null plan");
+  return host_attention(p, dtype, Q, K, V, idx, counts, out_dtype, out, lse, visits);
+}
+
+int fpb_host_dense_attention(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                             const void* V, fpb_dtype out_dtype, void* out, float* lse) {
+  return host_attention(p, dtype, Q, K, V, nullptr, nullptr, out_dtype, out, lse, nullptr);
+}
+
+int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                     const void* V, fpb_dtype out_dtype, void* out, float* lse, int32_t* idx,
+                     int32_t* counts, unsigned long long* visits) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc || (rc = check_dtype(dtype)) || (rc = check_dtype(out_dtype))) return rc;
+  if (!Q || !K || !V || !out || !lse) return fail(FPB_EUSAGE, "null pointer");
+  const size_t qb = q_elems(D) * dsz(dtype), kb = kv_elems(D) * dsz(dtype),
+               ob = q_elems(D) * dsz(out_dtype), lb = (size_t)D.Z * D.Hq * D.L * 4,
+               ib = map_elems(D) * 4, cb = (size_t)D.Z * D.M * D.Hq * 4;
+  const size_t wsd = ws_discover(D, dtype), wsa = ws_attention(D, dtype);
+  const size_t wsb = wsd > wsa ? wsd : wsa;
+  const size_t need = align_up(qb) + 2 * align_up(kb) + align_up(ob) + align_up(lb) +
+                      align_up(ib) + align_up(cb) + align_up(wsb) + 2048;
+  uint8_t* base;
+  cudaStream_t st;
+  if ((rc = arena_get(need, &base, &st))) return rc;
+  Carve c{base};
+  void* dq = c.take<void>(qb);
+  void* dk = c.take<void>(kb);
+  void* dv = c.take<void>(kb);
+  void* dout = c.take<void>(ob);
+  float* dl = c.take<float>(lb);
+  int32_t* di = c.take<int32_t>(ib);
+  int32_t* dc = c.take<int32_t>(cb);
+  unsigned long long* dvis = c.take<unsigned long long>(8);
+  void* ws = c.take<void>(wsb);
+  FPB_CUDA(cudaMemcpyAsync(dq, Q, qb, cudaMemcpyHostToDevice, st));
+  FPB_CUDA(cudaMemcpyAsync(dk, K, kb, cudaMemcpyHostToDevice, st));
+  FPB_CUDA(cudaMemcpyAsync(dv, V, kb, cudaMemcpyHostToDevice, st));
+  FPB_CUDA(cudaMemsetAsync(dvis, 0, 8, st));
+  if ((rc = fpb_discover_select(p, dtype, dq, dk, nullptr, nullptr, nullptr, nullptr, di, dc, ws,
+                                wsb, st)))
+    return rc;
+  if ((rc = fpb_block_sparse_attention(p, dtype, dq, dk, dv, di, dc, out_dtype, dout, dl, dvis,
+                                       nullptr, ws, wsb, st)))
+    return rc;
+  FPB_CUDA(cudaMemcpyAsync(out, dout, ob, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaMemcpyAsync(lse, dl, lb, cudaMemcpyDeviceToHost, st));
+  if (idx) FPB_CUDA(cudaMemcpyAsync(idx, di, ib, cudaMemcpyDeviceToHost, st));
+  if (counts) FPB_CUDA(cudaMemcpyAsync(counts, dc, cb, cudaMemcpyDeviceToHost, st));
+  unsigned long long vis = 0;
+  FPB_CUDA(cudaMemcpyAsync(&vis, dvis, 8, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaStreamSynchronize(st));
+  if (visits) *visits += vis;
+  return FPB_OK;
+}
+
+}  // extern "C"

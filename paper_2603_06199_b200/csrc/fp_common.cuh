@@ -1,0 +1,74 @@
+// fp_common.cuh — shared definitions for the FlashPrefill sm_100a kernels.
+#pragma once
+
+#include <cfloat>
+#include <cstdint>
+
+#include "fp_ptx.cuh"
+
+namespace fpb {
+
+constexpr int kBlock = 128;      // B: token block == MMA tile edge (core.hpp:88)
+constexpr int kHeadDim = 128;    // d
+constexpr float kLog2e = 1.4426950408889634f;  // core.hpp:13
+constexpr float kNegSentinel = -FLT_MAX;       // discovery.hpp:12
+
+// Shapes + PipelineConfig resolved on the host (core.hpp:96-111).
+struct Dims {
+  int Z, Hq, Hkv, L, M;     // M == N == ceil(L / B)
+  int group;                // Hq / Hkv
+  int last_len;             // length of block M-1
+  float to_bits;            // tau * log2(e)
+  float eps, alpha;
+  int sink_blocks, window_blocks;
+};
+
+__host__ __device__ __forceinline__ int block_len(const Dims& D, int blk) {
+  return blk + 1 == D.M ? D.last_len : kBlock;
+}
+
+// Block-wide reductions over `nthreads` (multiple of 32) threads using `scratch` (>= 32 floats).
+template <int kThreads>
+__device__ __forceinline__ float block_max(float v, float* scratch) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) scratch[w] = v;
+  __syncthreads();
+  v = (l < kThreads / 32) ? scratch[l] : -INFINITY;
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <int kThreads>
+__device__ __forceinline__ float block_sum(float v, float* scratch) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) scratch[w] = v;
+  __syncthreads();
+  v = (l < kThreads / 32) ? scratch[l] : 0.0f;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+// Exclusive prefix count of `pred` across the block (ascending thread order); returns the slot and
+// writes the block total to *total.
+template <int kThreads>
+__device__ __forceinline__ int block_prefix_count(bool pred, int* scratch, int* total) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const unsigned bal = __ballot_sync(0xffffffffu, pred);
+  const int in_warp = __popc(bal & ((1u << l) - 1u));
+  __syncthreads();
+  if (l == 0) scratch[w] = __popc(bal);
+  __syncthreads();
+  int before = 0, all = 0;
+#pragma unroll
+  for (int i = 0; i < kThreads / 32; ++i) {
+    const int c = scratch[i];
+    before += (i < w) ? c : 0;
+    all += c;
+  }
+  *total = all;
+  return before + in_warp;
+}
+
+}  // namespace fpb

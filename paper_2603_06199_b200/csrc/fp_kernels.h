@@ -1,0 +1,53 @@
+// fp_kernels.h — host-side launchers of the sm_100a kernels (internal to libfpb200.so).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "fp_common.cuh"
+
+namespace fpb {
+
+// pool.cu
+cudaError_t launch_pool_keys(const Dims& D, bool bf16_in, const void* K, float* pooled,
+                             __nv_bfloat16* kbar_split, cudaStream_t s);
+cudaError_t launch_split_pooled(const Dims& D, const float* pooled, __nv_bfloat16* kbar_split,
+                                cudaStream_t s);
+cudaError_t launch_f32_to_bf16(const float* src, __nv_bfloat16* hi, __nv_bfloat16* lo, size_t n,
+                               cudaStream_t s);
+
+// select.cu
+cudaError_t launch_normalize(const Dims& D, const float* energy, const float* local_max,
+                             float* score, cudaStream_t s);
+cudaError_t launch_threshold(const Dims& D, const float* score, uint8_t* mask,
+                             unsigned long long* comparisons, cudaStream_t s);
+cudaError_t launch_compress(const Dims& D, const uint8_t* mask, int32_t* idx, int32_t* counts,
+                            cudaStream_t s);
+cudaError_t launch_visit_count(const Dims& D, const int32_t* counts, unsigned long long* total,
+                               cudaStream_t s);
+cudaError_t launch_full_causal_plan(const Dims& D, int32_t* idx, int32_t* counts, cudaStream_t s);
+
+// discover.cu — fused block approximation (+ normalisation, + optional threshold/compaction).
+struct DiscoverOut {
+  float* energy = nullptr;
+  float* local_max = nullptr;
+  float* score = nullptr;
+  uint8_t* mask = nullptr;
+  int32_t* idx = nullptr;
+  int32_t* counts = nullptr;
+  bool normalize = true;  // false: only energy/local_max (approx_block_scores)
+};
+cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_planes,
+                            const __nv_bfloat16* kbar_split, const DiscoverOut& out,
+                            cudaStream_t s);
+
+// attention.cu — block-sparse (idx/counts) or dense-causal (idx == nullptr) tcgen05 attention.
+cudaError_t launch_attention(const Dims& D, const __nv_bfloat16* Q, const __nv_bfloat16* K,
+                             const __nv_bfloat16* V, const int32_t* idx, const int32_t* counts,
+                             bool out_bf16, void* out, float* lse, unsigned long long* visits,
+                             int32_t* plan_error, cudaStream_t s);
+
+// tensor maps (abi.cu)
+bool make_tmap_rows128(CUtensorMap* map, const void* base, uint64_t rows, uint64_t planes);
+
+}  // namespace fpb

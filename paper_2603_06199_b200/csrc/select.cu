@@ -1,0 +1,149 @@
+// select.cu — standalone kernels for the unfused API entry points:
+//   normalize_block_scores (discovery.hpp:119-148), max_threshold_mask (selection.hpp:63-92),
+//   compress_indices (selection.hpp:176-192), visit_count (selection.hpp:195-200),
+//   full_causal_plan (attention.hpp:178-192).
+// All are HBM-bound integer/compare work: one warp per score row, warp-level reductions, ballot
+// compaction.  max/compare/compaction are exact, so given the same score map the mask, idx and
+// counts are bit-identical to the reference.  The fused hot path (discover.cu) does the same work
+// in the epilogue of the discovery kernel instead.
+#include "fp_kernels.h"
+
+namespace fpb {
+
+__device__ __forceinline__ float warp_max(float v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One warp per (z, h, i) row.
+__global__ void normalize_kernel(Dims D, const float* __restrict__ energy,
+                                 const float* __restrict__ local_max, float* __restrict__ score) {
+  const long row = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long rows = (long)D.Z * D.Hq * D.M;
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int i = (int)(row % D.M), N = D.M;
+  const float* en = energy + row * N;
+  const float* lm = local_max + row * N;
+  float* dst = score + row * N;
+  float rmax = kNegSentinel;
+  for (int j = lane; j <= i; j += 32) rmax = fmaxf(rmax, lm[j]);
+  rmax = warp_max(rmax);
+  float total = 0.f;
+  for (int j = lane; j <= i; j += 32) total += en[j] * exp2f(lm[j] - rmax);
+  total = warp_sum(total);
+  const float inv = 1.0f / (total + D.eps);
+  for (int j = lane; j < N; j += 32) dst[j] = (j <= i) ? (en[j] * exp2f(lm[j] - rmax)) * inv : 0.f;
+}
+
+cudaError_t launch_normalize(const Dims& D, const float* energy, const float* local_max,
+                             float* score, cudaStream_t s) {
+  const long rows = (long)D.Z * D.Hq * D.M;
+  normalize_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(D, energy, local_max, score);
+  return cudaGetLastError();
+}
+
+// One warp per (z, h, i) score row; writes the head-last mask row mask[z, i, :, h].
+__global__ void threshold_kernel(Dims D, const float* __restrict__ score, uint8_t* __restrict__ mask,
+                                 unsigned long long* __restrict__ comparisons) {
+  const long row = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long rows = (long)D.Z * D.Hq * D.M;
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int i = (int)(row % D.M), N = D.M;
+  const int h = (int)((row / D.M) % D.Hq), z = (int)(row / ((long)D.M * D.Hq));
+  const float* srow = score + row * N;
+  float max_val = 0.0f;  // selection.hpp:75 — initialised to 0, not -inf
+  for (int j = lane; j <= i; j += 32) max_val = fmaxf(max_val, srow[j]);
+  max_val = warp_max(max_val);
+  const float thresh = D.alpha * max_val;  // selection.hpp:80
+  uint8_t* mrow = mask + ((size_t)z * D.M + i) * (size_t)N * D.Hq + h;
+  for (int j = lane; j < N; j += 32) {
+    uint8_t a = 0;
+    if (j <= i)
+      a = (srow[j] >= thresh) || j < D.sink_blocks || (i - j) < D.window_blocks;  // :82-84
+    mrow[(size_t)j * D.Hq] = a;
+  }
+  if (comparisons && lane == 0) atomicAdd(comparisons, 2ull * (unsigned long long)(i + 1));
+}
+
+cudaError_t launch_threshold(const Dims& D, const float* score, uint8_t* mask,
+                             unsigned long long* comparisons, cudaStream_t s) {
+  const long rows = (long)D.Z * D.Hq * D.M;
+  threshold_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(D, score, mask, comparisons);
+  return cudaGetLastError();
+}
+
+// One warp per (z, i, h): ballot-compaction of active j in ascending order, then the fill value N.
+__global__ void compress_kernel(Dims D, const uint8_t* __restrict__ mask, int32_t* __restrict__ idx,
+                                int32_t* __restrict__ counts) {
+  const long row = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long rows = (long)D.Z * D.M * D.Hq;
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int h = (int)(row % D.Hq);
+  const long zi = row / D.Hq;
+  const int N = D.M, H = D.Hq;
+  const uint8_t* mrow = mask + (size_t)zi * N * H + h;
+  int32_t* irow = idx + (size_t)zi * N * H + h;
+  int base = 0;
+  for (int j0 = 0; j0 < N; j0 += 32) {
+    const int j = j0 + lane;
+    const bool a = j < N && mrow[(size_t)j * H] != 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, a);
+    if (a) irow[(size_t)(base + __popc(bal & ((1u << lane) - 1u))) * H] = j;
+    base += __popc(bal);
+  }
+  for (int slot = base + lane; slot < N; slot += 32) irow[(size_t)slot * H] = N;
+  if (lane == 0) counts[row] = base;
+}
+
+cudaError_t launch_compress(const Dims& D, const uint8_t* mask, int32_t* idx, int32_t* counts,
+                            cudaStream_t s) {
+  const long rows = (long)D.Z * D.M * D.Hq;
+  compress_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(D, mask, idx, counts);
+  return cudaGetLastError();
+}
+
+__global__ void visit_count_kernel(const int32_t* __restrict__ counts, size_t n,
+                                   unsigned long long* __restrict__ total) {
+  unsigned long long acc = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    acc += (unsigned long long)(long long)counts[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(total, acc);
+}
+
+cudaError_t launch_visit_count(const Dims& D, const int32_t* counts, unsigned long long* total,
+                               cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(total, 0, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  const size_t n = (size_t)D.Z * D.M * D.Hq;
+  visit_count_kernel<<<148, 256, 0, s>>>(counts, n, total);
+  return cudaGetLastError();
+}
+
+__global__ void full_plan_kernel(Dims D, int32_t* __restrict__ idx, int32_t* __restrict__ counts) {
+  const int N = D.M, H = D.Hq;
+  const size_t n = (size_t)D.Z * D.M * N * H;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const int h = (int)(e % H);
+    const int slot = (int)((e / H) % N);
+    const int i = (int)((e / ((size_t)H * N)) % D.M);
+    idx[e] = slot <= i ? slot : N;
+    if (slot == 0) counts[(e / ((size_t)H * N)) * H + h] = i + 1;
+  }
+}
+
+cudaError_t launch_full_causal_plan(const Dims& D, int32_t* idx, int32_t* counts, cudaStream_t s) {
+  full_plan_kernel<<<148 * 8, 256, 0, s>>>(D, idx, counts);
+  return cudaGetLastError();
+}
+
+}  // namespace fpb

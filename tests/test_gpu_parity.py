@@ -1,0 +1,241 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle on identical inputs.
+
+Bars (north_star / SURVEY §8c):
+  * pooled keys, threshold mask, compaction: bit-exact given identical inputs;
+  * discovery mask / idx / counts: bit-exact except blocks whose reference score lies within
+    MASK_EPS * thresh of the threshold (counted and reported);
+  * attention out: max-abs <= 2e-2 and mean-abs <= 1e-3 against the reference's fp32 result on the
+    same plan; lse compared in base 2 with the same bars.
+"""
+import numpy as np
+import pytest
+import torch
+
+from tests._util import (MASK_EPS, OUT_MAX_ABS, OUT_MEAN_ABS, bf16_round, compare_masks,
+                         composite_np, err, rows_with_near)
+
+pytestmark = pytest.mark.gpu
+
+
+def _cuda(x, dtype=torch.bfloat16):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda", dtype)
+
+
+def _np(t):
+    return t.detach().float().cpu().numpy() if t.dtype != torch.uint8 and t.dtype != torch.int32 \
+        else t.cpu().numpy()
+
+
+def _planted(port, kind, a, b, L, H=2, seed=3, strength=2.5):
+    q, k, v, _ = port.generate_planted(kind, strength, a, b, 0.5, seed, 1, H, L, 128, 128)
+    return bf16_round(q), bf16_round(k), bf16_round(v)
+
+
+# --------------------------------------------------------------------------- pooling (K1)
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("L", [128, 1000, 2048])
+def test_pool_keys_bitexact(fp, port, dtype, L):
+    rng = np.random.default_rng(L)
+    k = rng.normal(0, 1, (2, 3, L, 128)).astype(np.float32)
+    if dtype == torch.bfloat16:
+        k = bf16_round(k)
+    got = _np(fp.pool_keys(_cuda(k, dtype), fp.make_block_grid(L, 128)).data)
+    want = port.pool_keys(k, 128)
+    assert np.array_equal(got, want)
+
+
+# --------------------------------------------------------------------------- discovery (K2)
+@pytest.mark.parametrize("case", [(0, 3, 0, 2048), (1, 300, 0, 2048), (1, 777, 0, 1000),
+                                  (2, 9, 4, 1536), (3, 1500, 0, 4096)])
+def test_discover_maps(fp, port, case):
+    kind, a, b, L = case
+    q, k, v = _planted(port, kind, a, b, L)
+    tau = float(port.scale(128))
+    en, lm, sc = port.discover(q, k, 128, tau)
+    m = fp.discover(_cuda(q), _cuda(k), fp.make_block_grid(L, 128), tau)
+    gen, glm, gsc = _np(m.energy), _np(m.local_max), _np(m.score)
+    M = sc.shape[2]
+    tri = np.tril(np.ones((M, M), bool))[None, None]
+    # non-causal sentinels are exact (discovery.hpp:84, 124)
+    assert np.all(gen[:, :, ~tri[0, 0]] == 0) and np.all(gsc[:, :, ~tri[0, 0]] == 0)
+    assert np.all(glm[:, :, ~tri[0, 0]] == np.finfo(np.float32).min)
+    # causal entries: local max (base-2 logit units) and scores close to the fp32 reference
+    dl = np.abs(glm - lm)[np.broadcast_to(tri, lm.shape)]
+    assert dl.max() <= 2e-4 * max(1.0, np.abs(lm[np.broadcast_to(tri, lm.shape)]).max())
+    rs = np.abs(gsc - sc) / np.maximum(sc, 1e-30)
+    big = np.broadcast_to(tri, sc.shape) & (sc > 1e-6)
+    assert rs[big].max() <= 1e-3, rs[big].max()
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.05, 0.12, 0.5, 1.0])
+def test_threshold_and_compress_bitexact(fp, port, alpha):
+    q, k, _ = _planted(port, 1, 300, 0, 4096, H=3)
+    tau = float(port.scale(128))
+    _, _, sc = port.discover(q, k, 128, tau)
+    cfg = fp.PipelineConfig(alpha=alpha)
+    st = fp.SelectionStats()
+    gm = fp.max_threshold_mask(_cuda(sc, torch.float32), cfg, st)
+    mask, cmp = port.max_threshold_mask(sc, 128, alpha, 256, 512)
+    assert np.array_equal(_np(gm.active), mask)
+    assert st.score_comparisons == cmp
+    plan = fp.compress_indices(gm)
+    idx, counts = port.compress_indices(mask)
+    assert np.array_equal(_np(plan.indices), idx) and np.array_equal(_np(plan.counts), counts)
+    assert fp.visit_count(plan) == port.visit_count(counts)
+
+
+def test_compress_arbitrary_mask(fp, port):
+    rng = np.random.default_rng(5)
+    mask = (rng.random((2, 17, 17, 5)) < 0.3).astype(np.uint8)  # includes j > i entries
+    plan = fp.compress_indices(fp.ActiveMask(_cuda(mask, torch.uint8)))
+    idx, counts = port.compress_indices(mask)
+    assert np.array_equal(_np(plan.indices), idx) and np.array_equal(_np(plan.counts), counts)
+
+
+@pytest.mark.parametrize("shape", [(1, 2, 2, 2048), (1, 4, 2, 3000), (2, 2, 1, 1024),
+                                   (1, 8, 2, 4096)])
+@pytest.mark.parametrize("alpha", [0.05, 0.12, 0.3])
+def test_fused_discover_select(fp, port, shape, alpha):
+    Z, Hq, Hkv, L = shape
+    q, k, v = composite_np(11 + L, Z, Hq, Hkv, L)
+    q, k = bf16_round(q), bf16_round(k)
+    tau = float(port.scale(128))
+    _, _, sc = port.discover(q, k, 128, tau)
+    mask, _ = port.max_threshold_mask(sc, 128, alpha, 256, 512)
+    idx, counts = port.compress_indices(mask)
+    cfg = fp.PipelineConfig(alpha=alpha)
+    plan, smap, gmask = fp.discover_select(_cuda(q), _cuda(k), cfg, want_score=True,
+                                           want_mask=True)
+    bad, near, flipped = compare_masks(_np(gmask.active), mask, sc, alpha)
+    print(f"shape={shape} alpha={alpha}: near-threshold blocks={near} flipped={flipped}")
+    assert bad == 0
+    ok_rows = ~rows_with_near(sc, alpha)
+    gi, gc = _np(plan.indices), _np(plan.counts)
+    assert np.array_equal(gc[ok_rows], counts[ok_rows])
+    assert np.array_equal(gi.transpose(0, 1, 3, 2)[ok_rows], idx.transpose(0, 1, 3, 2)[ok_rows])
+
+
+# --------------------------------------------------------------------------- attention (K4/K5)
+def _attn_check(go, gl, ro, rl):
+    mx, mean = err(go, ro)
+    lmx, lmean = err(gl, rl)
+    print(f"out max {mx:.3e} mean {mean:.3e} | lse max {lmx:.3e} mean {lmean:.3e}")
+    assert mx <= OUT_MAX_ABS and mean <= OUT_MEAN_ABS
+    assert lmx <= OUT_MAX_ABS and lmean <= OUT_MEAN_ABS
+
+
+@pytest.mark.parametrize("shape", [(1, 2, 2, 1024), (1, 4, 2, 1000), (2, 2, 1, 640),
+                                   (1, 1, 1, 130)])
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_sparse_attention_same_plan(fp, port, shape, out_dtype):
+    Z, Hq, Hkv, L = shape
+    q, k, v = (bf16_round(x) for x in composite_np(7 + L, Z, Hq, Hkv, L))
+    tau = float(port.scale(128))
+    _, _, sc = port.discover(q, k, 128, tau)
+    mask, _ = port.max_threshold_mask(sc, 128, 0.12, 256, 512)
+    idx, counts = port.compress_indices(mask)
+    ro, rl, rvis = port.block_sparse_attention(q, k, v, idx, counts, 128, tau)
+    st = fp.AttentionStats()
+    res = fp.block_sparse_attention(_cuda(q), _cuda(k), _cuda(v),
+                                    fp.SparseBlockPlan(_cuda(idx, torch.int32),
+                                                       _cuda(counts, torch.int32)),
+                                    fp.make_block_grid(L, 128), tau, st, out_dtype=out_dtype)
+    assert st.block_visits == rvis
+    _attn_check(_np(res.out), _np(res.lse), ro, rl)
+
+
+@pytest.mark.parametrize("L", [128, 700, 1024, 2048])
+def test_dense_attention(fp, port, L):
+    q, k, v = (bf16_round(x) for x in composite_np(L, 1, 2, 1, L))
+    tau = float(port.scale(128))
+    ro, rl = port.dense_attention(q, k, v, tau)
+    res = fp.dense_attention(_cuda(q), _cuda(k), _cuda(v), tau, out_dtype=torch.float32)
+    _attn_check(_np(res.out), _np(res.lse), ro, rl)
+
+
+def test_full_plan_equals_dense(fp, port):
+    L = 1500
+    q, k, v = (bf16_round(x) for x in composite_np(2, 1, 2, 2, L))
+    tau = float(port.scale(128))
+    grid = fp.make_block_grid(L, 128)
+    plan = fp.full_causal_plan(1, 2, grid)
+    idx, counts = port.full_causal_plan(1, 2, grid.num_query_blocks)
+    assert np.array_equal(_np(plan.indices), idx) and np.array_equal(_np(plan.counts), counts)
+    a = fp.block_sparse_attention(_cuda(q), _cuda(k), _cuda(v), plan, grid, tau,
+                                  out_dtype=torch.float32)
+    b = fp.dense_attention(_cuda(q), _cuda(k), _cuda(v), tau, out_dtype=torch.float32)
+    assert err(_np(a.out), _np(b.out))[0] <= 1e-4 and err(_np(a.lse), _np(b.lse))[0] <= 1e-4
+
+
+def test_attention_edge_semantics(fp, port):
+    """count=0 -> NaN / -inf; listed j > i attended in full; PlanError on bad index."""
+    L = 512
+    q, k, v = (bf16_round(x) for x in composite_np(9, 1, 1, 1, L))
+    tau = float(port.scale(128))
+    M = 4
+    idx = np.full((1, M, M, 1), M, np.int32)
+    counts = np.zeros((1, M, 1), np.int32)
+    idx[0, 0, :2, 0] = [0, 3]   # row 0 lists a future block (attended in full)
+    counts[0, 0, 0] = 2
+    idx[0, 2, :1, 0] = [1]      # row 2 without its diagonal
+    counts[0, 2, 0] = 1
+    # rows 1 and 3 empty -> NaN / -inf
+    ro, rl, _ = port.block_sparse_attention(q, k, v, idx, counts, 128, tau)
+    res = fp.block_sparse_attention(_cuda(q), _cuda(k), _cuda(v),
+                                    fp.SparseBlockPlan(_cuda(idx, torch.int32),
+                                                       _cuda(counts, torch.int32)),
+                                    fp.make_block_grid(L, 128), tau, out_dtype=torch.float32)
+    go, gl = _np(res.out), _np(res.lse)
+    assert np.array_equal(np.isnan(go), np.isnan(ro))
+    assert np.array_equal(np.isneginf(gl), np.isneginf(rl))
+    fin = ~np.isnan(ro)
+    assert np.abs(go[fin] - ro[fin]).max() <= OUT_MAX_ABS
+    fin = np.isfinite(rl)
+    assert np.abs(gl[fin] - rl[fin]).max() <= OUT_MAX_ABS
+    bad = idx.copy()
+    bad[0, 0, 1, 0] = M  # fill value inside the counted prefix -> PlanError
+    with pytest.raises(fp.PlanError):
+        fp.block_sparse_attention(_cuda(q), _cuda(k), _cuda(v),
+                                  fp.SparseBlockPlan(_cuda(bad, torch.int32),
+                                                     _cuda(counts, torch.int32)),
+                                  fp.make_block_grid(L, 128), tau)
+
+
+def test_fp32_pipeline_c1_small(fp, port):
+    """fp32 inputs (config C1 style, reduced L): discovery split-precision + attention."""
+    L = 2048
+    q, k, v = composite_np(1, 1, 1, 1, L)
+    tau = float(port.scale(128))
+    _, _, sc = port.discover(q, k, 128, tau)
+    mask, _ = port.max_threshold_mask(sc, 128, 0.12, 256, 512)
+    idx, counts = port.compress_indices(mask)
+    cfg = fp.PipelineConfig()
+    plan, _, gmask = fp.discover_select(_cuda(q, torch.float32), _cuda(k, torch.float32), cfg,
+                                        want_mask=True)
+    bad, near, _ = compare_masks(_np(gmask.active), mask, sc, 0.12)
+    assert bad == 0
+    ro, rl, _ = port.block_sparse_attention(q, k, v, idx, counts, 128, tau)
+    res = fp.block_sparse_attention(_cuda(q, torch.float32), _cuda(k, torch.float32),
+                                    _cuda(v, torch.float32),
+                                    fp.SparseBlockPlan(_cuda(idx, torch.int32),
+                                                       _cuda(counts, torch.int32)),
+                                    fp.make_block_grid(L, 128), tau)
+    _attn_check(_np(res.out), _np(res.lse), ro, rl)
+
+
+def test_prefill_host_e2e(fp, port):
+    L = 2048
+    q, k, v = (bf16_round(x) for x in composite_np(21, 1, 4, 2, L))
+    tau = float(port.scale(128))
+    cfg = fp.PipelineConfig()
+    qh, kh, vh = (torch.from_numpy(x).to(torch.bfloat16).pin_memory() for x in (q, k, v))
+    out = torch.empty(qh.shape, dtype=torch.float32).pin_memory()
+    lse = torch.empty(qh.shape[:3], dtype=torch.float32).pin_memory()
+    M = (L + 127) // 128
+    idx = torch.empty((1, M, M, 4), dtype=torch.int32)
+    counts = torch.empty((1, M, 4), dtype=torch.int32)
+    vis = fp.prefill_host(qh, kh, vh, cfg, out, lse, idx, counts)
+    assert vis == int(counts.sum())
+    ro, rl, rvis = port.block_sparse_attention(q, k, v, idx.numpy(), counts.numpy(), 128, tau)
+    assert rvis == vis
+    _attn_check(out.numpy(), lse.numpy(), ro, rl)

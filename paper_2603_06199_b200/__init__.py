@@ -12,3 +12,4 @@ from .bsattn import (  # noqa: F401
     flops_sparse, full_causal_plan, make_block_grid, make_sequence_batch, max_threshold_mask,
     normalize_block_scores, pool_keys, prefill, prefill_host, visit_count,
 )
+from . import workload  # noqa: F401,E402  (synthetic inputs for bench / tests)

@@ -113,8 +113,10 @@ size_t ws_discover(const Dims& D, fpb_dtype t) {
   if (t == FPB_F32) b += align_up(2 * q_elems(D) * 2);
   return b;
 }
-size_t ws_attention(const Dims& D, fpb_dtype t) {
-  return t == FPB_F32 ? align_up(q_elems(D) * 2) + 2 * align_up(kv_elems(D) * 2) : 0;
+size_t ws_attention(const Dims& D, fpb_dtype t) {  // fp32: Q hi/lo, K hi/lo, V bf16
+  return t == FPB_F32 ? align_up(2 * q_elems(D) * 2) + align_up(2 * kv_elems(D) * 2) +
+                            align_up(kv_elems(D) * 2)
+                      : 0;
 }
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -325,17 +327,19 @@ static int attention_common(const fpb_problem* p, fpb_dtype dtype, const void* Q
   if (dtype == FPB_F32) {
     uint8_t* w = static_cast<uint8_t*>(workspace);
     __nv_bfloat16* q2 = reinterpret_cast<__nv_bfloat16*>(w);
-    __nv_bfloat16* k2 = reinterpret_cast<__nv_bfloat16*>(w + align_up(q_elems(D) * 2));
-    __nv_bfloat16* v2 = reinterpret_cast<__nv_bfloat16*>(w + align_up(q_elems(D) * 2) +
-                                                         align_up(kv_elems(D) * 2));
-    FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(Q), q2, nullptr, q_elems(D), S(stream)));
-    FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(K), k2, nullptr, kv_elems(D), S(stream)));
+    __nv_bfloat16* k2 = reinterpret_cast<__nv_bfloat16*>(w + align_up(2 * q_elems(D) * 2));
+    __nv_bfloat16* v2 = reinterpret_cast<__nv_bfloat16*>(w + align_up(2 * q_elems(D) * 2) +
+                                                         align_up(2 * kv_elems(D) * 2));
+    FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(Q), q2, q2 + q_elems(D), q_elems(D),
+                                S(stream)));
+    FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(K), k2, k2 + kv_elems(D), kv_elems(D),
+                                S(stream)));
     FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(V), v2, nullptr, kv_elems(D), S(stream)));
     q = q2;
     k = k2;
     v = v2;
   }
-  FPB_CUDA(launch_attention(D, q, k, v, idx, counts, out_dtype == FPB_BF16, out, lse, visits,
+  FPB_CUDA(launch_attention(D, dtype == FPB_F32 ? 2 : 1, q, k, v, idx, counts, out_dtype == FPB_BF16, out, lse, visits,
                             plan_error, S(stream)));
   return FPB_OK;
 }

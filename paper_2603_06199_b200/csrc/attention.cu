@@ -24,7 +24,11 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kTile = kBlock * kHeadDim * 2;  // 32 KiB bf16 tile
-constexpr int kKStages = 3, kVStages = 2;
+constexpr int kVStages = 2;
+// bf16 inputs: one K tile per block, 3-slot ring.  fp32 inputs (NS = 2): Q and K are fed as bf16
+// hi + lo splits (S = Qh Kh + Ql Kh + Qh Kl, ~fp32 logits); two K tiles per block, 2-slot ring.
+template <int NS>
+constexpr int k_slots() { return NS == 1 ? 3 : 2; }
 constexpr float kRescaleThreshold = 8.0f;     // log2 units
 
 struct AttnParams {
@@ -38,8 +42,10 @@ struct AttnParams {
   int out_bf16;
 };
 
+template <int NS>
 struct AttnSmem {
-  uint8_t q[kTile];
+  static constexpr int kKStages = k_slots<NS>();
+  uint8_t q[NS][kTile];
   uint8_t k[kKStages][kTile];
   uint8_t v[kVStages][kTile];
   uint64_t q_full;
@@ -53,12 +59,15 @@ struct AttnSmem {
   // followed by int list[M] (dynamic)
 };
 
+template <int NS>
 __global__ void __launch_bounds__(kThreads, 1)
     attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const AttnParams prm) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  auto& s = *reinterpret_cast<AttnSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                         ~uintptr_t(1023));
+  using Smem = AttnSmem<NS>;
+  constexpr int kKStages = Smem::kKStages;
+  auto& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                     ~uintptr_t(1023));
   int* list = reinterpret_cast<int*>(&s + 1);
   const Dims& D = prm.D;
   const int N = D.M;
@@ -134,20 +143,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();
       const uint32_t qb = smem_u32(&s.q_full);
-      mbar_arrive_expect_tx(qb, kTile);
-      for (int a = 0; a < 2; ++a)
-        tma_load_3d_hint(smem_u32(s.q) + a * (kTile / 2), &tm_q, qb, a * 64, qi * kBlock,
-                         z * D.Hq + h, pol_q);
+      mbar_arrive_expect_tx(qb, NS * kTile);
+      for (int sp = 0; sp < NS; ++sp)
+        for (int a = 0; a < 2; ++a)
+          tma_load_3d_hint(smem_u32(s.q[sp]) + a * (kTile / 2), &tm_q, qb, a * 64, qi * kBlock,
+                           sp * D.Z * D.Hq + z * D.Hq + h, pol_q);
       for (int n = 0; n <= nblk; ++n) {
-        if (n < nblk) {
-          const int st = n % kKStages;
-          if (n >= kKStages) mbar_wait(smem_u32(&s.k_empty[st]), ((n / kKStages) - 1) & 1);
+        for (int sp = 0; n < nblk && sp < NS; ++sp) {
+          const int item = n * NS + sp;
+          const int st = item % kKStages;
+          if (item >= kKStages) mbar_wait(smem_u32(&s.k_empty[st]), ((item / kKStages) - 1) & 1);
           const uint32_t fb = smem_u32(&s.k_full[st]);
           mbar_arrive_expect_tx(fb, kTile);
           const int row = kv_of(n) * kBlock;
           for (int a = 0; a < 2; ++a)
-            tma_load_3d_hint(smem_u32(s.k[st]) + a * (kTile / 2), &tm_k, fb, a * 64, row, zkv,
-                             pol_kv);
+            tma_load_3d_hint(smem_u32(s.k[st]) + a * (kTile / 2), &tm_k, fb, a * 64, row,
+                             sp * D.Z * D.Hkv + zkv, pol_kv);
         }
         if (n >= 1) {
           const int m = n - 1;
@@ -185,19 +196,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(smem_u32(&s.o_ready));
       };
       for (int n = 0; n < nblk; ++n) {
-        const int b = n & 1, st = n % kKStages;
+        const int b = n & 1;
         if (n >= 2) mbar_wait(smem_u32(&s.s_free[b]), ((n >> 1) - 1) & 1);
-        mbar_wait(smem_u32(&s.k_full[st]), (n / kKStages) & 1);
-        tc_fence_after();
         const uint32_t s_tmem = tmem + b * 128;
-        const uint32_t qbase = smem_u32(s.q), kbase = smem_u32(s.k[st]);
+        for (int sp = 0; sp < NS; ++sp) {  // sp 0: K hi (x Q hi [+ Q lo]); sp 1: K lo (x Q hi)
+          const int item = n * NS + sp;
+          const int st = item % kKStages;
+          mbar_wait(smem_u32(&s.k_full[st]), (item / kKStages) & 1);
+          tc_fence_after();
+          const uint32_t kbase = smem_u32(s.k[st]);
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          const uint32_t off = (ks >> 2) * (kTile / 2) + (ks & 3) * 32;
-          mma_bf16_ss(s_tmem, sdesc_sw128(qbase + off, 16, 1024),
-                      sdesc_sw128(kbase + off, 16, 1024), idesc_qk, ks > 0 ? 1u : 0u);
+          for (int ks = 0; ks < 8; ++ks) {
+            const uint32_t off = (ks >> 2) * (kTile / 2) + (ks & 3) * 32;
+            const uint64_t kd = sdesc_sw128(kbase + off, 16, 1024);
+            mma_bf16_ss(s_tmem, sdesc_sw128(smem_u32(s.q[0]) + off, 16, 1024), kd, idesc_qk,
+                        (sp > 0 || ks > 0) ? 1u : 0u);
+            if (NS == 2 && sp == 0)
+              mma_bf16_ss(s_tmem, sdesc_sw128(smem_u32(s.q[1]) + off, 16, 1024), kd, idesc_qk, 1u);
+          }
+          mma_commit(smem_u32(&s.k_empty[st]));
         }
-        mma_commit(smem_u32(&s.k_empty[st]));
         mma_commit(smem_u32(&s.s_full[b]));
         if (n >= 1) issue_pv(n - 1);
       }
@@ -321,25 +339,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-}  // namespace
-
-cudaError_t launch_attention(const Dims& D, const __nv_bfloat16* Q, const __nv_bfloat16* K,
-                             const __nv_bfloat16* V, const int32_t* idx, const int32_t* counts,
-                             bool out_bf16, void* out, float* lse, unsigned long long* visits,
-                             int32_t* plan_error, cudaStream_t s) {
-  CUtensorMap tm_q, tm_k, tm_v;
-  if (!make_tmap_rows128(&tm_q, Q, D.L, (uint64_t)D.Z * D.Hq) ||
-      !make_tmap_rows128(&tm_k, K, D.L, (uint64_t)D.Z * D.Hkv) ||
-      !make_tmap_rows128(&tm_v, V, D.L, (uint64_t)D.Z * D.Hkv))
-    return cudaErrorInvalidValue;
-  AttnParams prm{D, idx, counts, out, lse, visits, plan_error, out_bf16 ? 1 : 0};
-  const size_t smem = sizeof(AttnSmem) + 1024 + sizeof(int) * (size_t)D.M;
-  cudaError_t e = cudaFuncSetAttribute(attention_kernel,
+template <int NS>
+cudaError_t launch_ns(const Dims& D, const CUtensorMap& tm_q, const CUtensorMap& tm_k,
+                      const CUtensorMap& tm_v, const AttnParams& prm, cudaStream_t s) {
+  const size_t smem = sizeof(AttnSmem<NS>) + 1024 + sizeof(int) * (size_t)D.M;
+  cudaError_t e = cudaFuncSetAttribute(attention_kernel<NS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const dim3 grid((unsigned)((size_t)D.Z * D.Hq * D.M));
-  attention_kernel<<<grid, kThreads, smem, s>>>(tm_q, tm_k, tm_v, prm);
+  attention_kernel<NS><<<grid, kThreads, smem, s>>>(tm_q, tm_k, tm_v, prm);
   return cudaGetLastError();
+}
+
+}  // namespace
+
+// Q / K: `splits` bf16 planes each ([hi][lo] for fp32 inputs); V: one bf16 plane.
+cudaError_t launch_attention(const Dims& D, int splits, const __nv_bfloat16* Q,
+                             const __nv_bfloat16* K, const __nv_bfloat16* V, const int32_t* idx,
+                             const int32_t* counts, bool out_bf16, void* out, float* lse,
+                             unsigned long long* visits, int32_t* plan_error, cudaStream_t s) {
+  CUtensorMap tm_q, tm_k, tm_v;
+  if (!make_tmap_rows128(&tm_q, Q, D.L, (uint64_t)splits * D.Z * D.Hq) ||
+      !make_tmap_rows128(&tm_k, K, D.L, (uint64_t)splits * D.Z * D.Hkv) ||
+      !make_tmap_rows128(&tm_v, V, D.L, (uint64_t)D.Z * D.Hkv))
+    return cudaErrorInvalidValue;
+  AttnParams prm{D, idx, counts, out, lse, visits, plan_error, out_bf16 ? 1 : 0};
+  return splits == 2 ? launch_ns<2>(D, tm_q, tm_k, tm_v, prm, s)
+                     : launch_ns<1>(D, tm_q, tm_k, tm_v, prm, s);
 }
 
 }  // namespace fpb

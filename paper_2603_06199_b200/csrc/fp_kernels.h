@@ -42,8 +42,8 @@ cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_
                             cudaStream_t s);
 
 // attention.cu — block-sparse (idx/counts) or dense-causal (idx == nullptr) tcgen05 attention.
-cudaError_t launch_attention(const Dims& D, const __nv_bfloat16* Q, const __nv_bfloat16* K,
-                             const __nv_bfloat16* V, const int32_t* idx, const int32_t* counts,
+cudaError_t launch_attention(const Dims& D, int splits, const __nv_bfloat16* Q,
+                             const __nv_bfloat16* K, const __nv_bfloat16* V, const int32_t* idx, const int32_t* counts,
                              bool out_bf16, void* out, float* lse, unsigned long long* visits,
                              int32_t* plan_error, cudaStream_t s);
 

@@ -1,0 +1,85 @@
+"""Multi-GPU partitioning of the FlashPrefill path.
+
+Every (z, Q head) is independent through discovery, selection and attention
+(discovery.hpp:87-88, selection.hpp:71-72, attention.hpp:59-60), so the path shards with no
+data-path collective:
+
+* ``kv_group_shard`` — strong scaling of one batch by KV-head groups: rank g owns KV heads
+  [g*Hkv/G, (g+1)*Hkv/G) and their Q heads; with G > Hkv each group's Q heads are split over
+  G/Hkv ranks and the KV head is replicated (e.g. Qwen3 Hkv=4 on 8 GPUs: 4 Q heads per rank).
+* ``unit_shard`` — weak scaling: work units (sequence, KV-head group) dealt contiguously.
+* ``gather_heads`` — the only collective: one all-gather of O and LSE along the head axis after
+  all kernels complete (NCCL over NVLink in production, gloo in the CPU tests).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+
+@dataclass(frozen=True)
+class HeadShard:
+    q_lo: int
+    q_hi: int
+    kv_lo: int
+    kv_hi: int
+
+    @property
+    def hq(self) -> int:
+        return self.q_hi - self.q_lo
+
+    @property
+    def hkv(self) -> int:
+        return self.kv_hi - self.kv_lo
+
+
+def kv_group_shard(Hq: int, Hkv: int, world: int, rank: int) -> HeadShard:
+    if Hq % Hkv:
+        raise ValueError("Hq must be a multiple of Hkv")
+    g = Hq // Hkv
+    if world <= Hkv:
+        if Hkv % world:
+            raise ValueError(f"{world} ranks do not divide {Hkv} KV heads")
+        per = Hkv // world
+        return HeadShard(rank * per * g, (rank + 1) * per * g, rank * per, (rank + 1) * per)
+    if world % Hkv or g % (world // Hkv):
+        raise ValueError(f"{world} ranks cannot split {Hkv} KV groups of {g} Q heads")
+    split = world // Hkv  # ranks per KV group
+    kv = rank // split
+    per_q = g // split
+    q0 = kv * g + (rank % split) * per_q
+    return HeadShard(q0, q0 + per_q, kv, kv + 1)
+
+
+def unit_shard(n_units: int, world: int, rank: int) -> range:
+    per, extra = divmod(n_units, world)
+    lo = rank * per + min(rank, extra)
+    return range(lo, lo + per + (1 if rank < extra else 0))
+
+
+def local_slices(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, s: HeadShard):
+    """Contiguous per-rank head slices of Z x H x L x d tensors."""
+    return (q[:, s.q_lo:s.q_hi].contiguous(), k[:, s.kv_lo:s.kv_hi].contiguous(),
+            v[:, s.kv_lo:s.kv_hi].contiguous())
+
+
+def gather_heads(out_local: torch.Tensor, lse_local: torch.Tensor, Hq: int, Hkv: int,
+                 group=None):
+    """All-gather per-rank (Z x hq_local x L x d, Z x hq_local x L) along the head axis."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    Z, hl, L, d = out_local.shape
+    # head-major staging so one all_gather_into_tensor moves every rank's block contiguously
+    ob = torch.empty((world * Z, hl, L, d), dtype=out_local.dtype, device=out_local.device)
+    lb = torch.empty((world * Z, hl, L), dtype=lse_local.dtype, device=lse_local.device)
+    dist.all_gather_into_tensor(ob, out_local.contiguous(), group=group)
+    dist.all_gather_into_tensor(lb, lse_local.contiguous(), group=group)
+    ob, lb = ob.view(world, Z, hl, L, d), lb.view(world, Z, hl, L)
+    order = [kv_group_shard(Hq, Hkv, world, r).q_lo for r in range(world)]
+    out = torch.empty((Z, Hq, L, d), dtype=out_local.dtype, device=out_local.device)
+    lse = torch.empty((Z, Hq, L), dtype=lse_local.dtype, device=lse_local.device)
+    for r, q0 in enumerate(order):
+        out[:, q0:q0 + hl] = ob[r]
+        lse[:, q0:q0 + hl] = lb[r]
+    return out, lse

@@ -239,3 +239,50 @@ def test_prefill_host_e2e(fp, port):
     ro, rl, rvis = port.block_sparse_attention(q, k, v, idx.numpy(), counts.numpy(), 128, tau)
     assert rvis == vis
     _attn_check(out.numpy(), lse.numpy(), ro, rl)
+
+
+# --------------------------------------------------------------------------- committed goldens
+def _golden_cases():
+    import glob
+    import os
+    return sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "gpu_*.npz")))
+
+
+@pytest.mark.parametrize("path", _golden_cases())
+def test_golden_reference_vectors(fp, port, path):
+    """CUDA path vs outputs produced by the unmodified reference (tests/golden/gen_golden.py)."""
+    g = np.load(path)
+    kind, strength, a, b, noise, seed, Z, H, L, d, B, bf = g["params"]
+    q, k, v, _ = port.generate_planted(int(kind), float(strength), int(a), int(b), float(noise),
+                                       int(seed), int(Z), int(H), int(L), int(d), int(B))
+    q, k, v = bf16_round(q), bf16_round(k), bf16_round(v)
+    L = int(L)
+    grid = fp.make_block_grid(L, 128)
+    tau = float(port.scale(128))
+    assert np.array_equal(_np(fp.pool_keys(_cuda(k), grid).data), g["pooled"])
+    for al in (0.0, 0.12, 0.5):
+        tag = f"a{int(al * 100):03d}"
+        plan, smap, gm = fp.discover_select(_cuda(q), _cuda(k), fp.PipelineConfig(alpha=al),
+                                            want_score=True, want_mask=True)
+        bad, near, _ = compare_masks(_np(gm.active), g[f"mask_{tag}"], g["score"], al)
+        assert bad == 0
+        ok = ~rows_with_near(g["score"], al)
+        assert np.array_equal(_np(plan.counts)[ok], g[f"counts_{tag}"][ok])
+        # standalone threshold/compaction on the reference's own score map: bit-exact
+        st = fp.SelectionStats()
+        m2 = fp.max_threshold_mask(_cuda(g["score"], torch.float32), fp.PipelineConfig(alpha=al), st)
+        assert np.array_equal(_np(m2.active), g[f"mask_{tag}"])
+        assert st.score_comparisons == int(g[f"cmp_{tag}"][0])
+        p2 = fp.compress_indices(m2)
+        assert np.array_equal(_np(p2.indices), g[f"idx_{tag}"])
+        assert np.array_equal(_np(p2.counts), g[f"counts_{tag}"])
+    st = fp.AttentionStats()
+    res = fp.block_sparse_attention(_cuda(q), _cuda(k), _cuda(v),
+                                    fp.SparseBlockPlan(_cuda(g["idx_a012"], torch.int32),
+                                                       _cuda(g["counts_a012"], torch.int32)),
+                                    grid, tau, st, out_dtype=torch.float32)
+    assert st.block_visits == int(g["visits"][0])
+    _attn_check(_np(res.out), _np(res.lse), g["out_sparse"], g["lse_sparse"])
+    if "out_dense" in g.files:
+        res = fp.dense_attention(_cuda(q), _cuda(k), _cuda(v), tau, out_dtype=torch.float32)
+        _attn_check(_np(res.out), _np(res.lse), g["out_dense"], g["lse_dense"])

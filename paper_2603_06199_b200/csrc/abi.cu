@@ -106,12 +106,23 @@ size_t kv_elems(const Dims& D) { return (size_t)D.Z * D.Hkv * D.L * kHeadDim; }
 size_t map_elems(const Dims& D) { return (size_t)D.Z * D.Hq * D.M * D.M; }
 size_t kbar_split_bytes(const Dims& D) { return 2ull * D.Z * D.Hkv * D.M * kHeadDim * 2; }
 
-// Workspace layouts.  discover: [kbar split][Q hi/lo planes if fp32]
-//                     attention: [Q bf16][K bf16][V bf16] if fp32
+// Workspace layouts.  discover: [scheduler counter][kbar split][Q hi/lo planes if fp32]
+//                     attention: [Q hi/lo][K hi/lo][V bf16] if fp32
+constexpr size_t kSchedBytes = 1024;
 size_t ws_discover(const Dims& D, fpb_dtype t) {
-  size_t b = align_up(kbar_split_bytes(D));
+  size_t b = kSchedBytes + align_up(kbar_split_bytes(D));
   if (t == FPB_F32) b += align_up(2 * q_elems(D) * 2);
   return b;
+}
+struct DiscWs {
+  int* sched;
+  __nv_bfloat16* kbar;
+  __nv_bfloat16* qplanes;  // fp32 inputs only
+};
+DiscWs disc_ws(const Dims& D, void* ws) {
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  return {reinterpret_cast<int*>(w), reinterpret_cast<__nv_bfloat16*>(w + kSchedBytes),
+          reinterpret_cast<__nv_bfloat16*>(w + kSchedBytes + align_up(kbar_split_bytes(D)))};
 }
 size_t ws_attention(const Dims& D, fpb_dtype t) {  // fp32: Q hi/lo, K hi/lo, V bf16
   return t == FPB_F32 ? align_up(2 * q_elems(D) * 2) + align_up(2 * kv_elems(D) * 2) +
@@ -129,17 +140,14 @@ int need_ws(size_t have, size_t need, void* ws) {
 
 // Discovery front half: pool k̄ (+split) and stage Q planes; returns the Q plane pointer.
 int discover_prepare(const Dims& D, fpb_dtype t, const void* Q, const void* K, float* pooled,
-                     void* ws, cudaStream_t st, __nv_bfloat16** kbar_split,
-                     const __nv_bfloat16** q_planes) {
-  uint8_t* w = static_cast<uint8_t*>(ws);
-  *kbar_split = reinterpret_cast<__nv_bfloat16*>(w);
-  FPB_CUDA(launch_pool_keys(D, t == FPB_BF16, K, pooled, *kbar_split, st));
+                     const DiscWs& w, cudaStream_t st, const __nv_bfloat16** q_planes) {
+  FPB_CUDA(launch_pool_keys(D, t == FPB_BF16, K, pooled, w.kbar, st));
   if (t == FPB_BF16) {
     *q_planes = static_cast<const __nv_bfloat16*>(Q);
   } else {
-    __nv_bfloat16* qp = reinterpret_cast<__nv_bfloat16*>(w + align_up(kbar_split_bytes(D)));
-    FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(Q), qp, qp + q_elems(D), q_elems(D), st));
-    *q_planes = qp;
+    FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(Q), w.qplanes, w.qplanes + q_elems(D),
+                                q_elems(D), st));
+    *q_planes = w.qplanes;
   }
   return FPB_OK;
 }
@@ -210,21 +218,19 @@ int fpb_approx_block_scores(const fpb_problem* p, fpb_dtype dtype, const void* Q
   if (rc || (rc = check_dtype(dtype))) return rc;
   if (!Q || !pooled || !energy || !local_max) return fail(FPB_EUSAGE, "null pointer");
   if ((rc = need_ws(workspace_bytes, ws_discover(D, dtype), workspace))) return rc;
-  uint8_t* w = static_cast<uint8_t*>(workspace);
-  __nv_bfloat16* kbar = reinterpret_cast<__nv_bfloat16*>(w);
-  FPB_CUDA(launch_split_pooled(D, pooled, kbar, S(stream)));
+  const DiscWs w = disc_ws(D, workspace);
+  FPB_CUDA(launch_split_pooled(D, pooled, w.kbar, S(stream)));
   const __nv_bfloat16* qp = static_cast<const __nv_bfloat16*>(Q);
   if (dtype == FPB_F32) {
-    __nv_bfloat16* q2 = reinterpret_cast<__nv_bfloat16*>(w + align_up(kbar_split_bytes(D)));
-    FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(Q), q2, q2 + q_elems(D), q_elems(D),
-                                S(stream)));
-    qp = q2;
+    FPB_CUDA(launch_f32_to_bf16(static_cast<const float*>(Q), w.qplanes, w.qplanes + q_elems(D),
+                                q_elems(D), S(stream)));
+    qp = w.qplanes;
   }
   DiscoverOut o;
   o.energy = energy;
   o.local_max = local_max;
   o.normalize = false;
-  FPB_CUDA(launch_discover(D, dtype == FPB_F32 ? 2 : 1, qp, kbar, o, S(stream)));
+  FPB_CUDA(launch_discover(D, dtype == FPB_F32 ? 2 : 1, qp, w.kbar, o, w.sched, S(stream)));
   return FPB_OK;
 }
 
@@ -248,9 +254,9 @@ int fpb_discover_select(const fpb_problem* p, fpb_dtype dtype, const void* Q, co
   if ((idx == nullptr) != (counts == nullptr))
     return fail(FPB_EUSAGE, "idx and counts must be given together");
   if ((rc = need_ws(workspace_bytes, ws_discover(D, dtype), workspace))) return rc;
-  __nv_bfloat16* kbar;
+  const DiscWs w = disc_ws(D, workspace);
   const __nv_bfloat16* qp;
-  if ((rc = discover_prepare(D, dtype, Q, K, nullptr, workspace, S(stream), &kbar, &qp))) return rc;
+  if ((rc = discover_prepare(D, dtype, Q, K, nullptr, w, S(stream), &qp))) return rc;
   DiscoverOut o;
   o.energy = energy;
   o.local_max = local_max;
@@ -258,7 +264,7 @@ int fpb_discover_select(const fpb_problem* p, fpb_dtype dtype, const void* Q, co
   o.mask = mask;
   o.idx = idx;
   o.counts = counts;
-  FPB_CUDA(launch_discover(D, dtype == FPB_F32 ? 2 : 1, qp, kbar, o, S(stream)));
+  FPB_CUDA(launch_discover(D, dtype == FPB_F32 ? 2 : 1, qp, w.kbar, o, w.sched, S(stream)));
   return FPB_OK;
 }
 

@@ -38,7 +38,7 @@ struct DiscoverOut {
   bool normalize = true;  // false: only energy/local_max (approx_block_scores)
 };
 cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_planes,
-                            const __nv_bfloat16* kbar_split, const DiscoverOut& out,
+                            const __nv_bfloat16* kbar_split, const DiscoverOut& out, int* sched,
                             cudaStream_t s);
 
 // attention.cu — block-sparse (idx/counts) or dense-causal (idx == nullptr) tcgen05 attention.

@@ -1,6 +1,6 @@
 // pool.cu — K1: block-mean key pooling (discovery.hpp:39-70) and operand conversions.
 //
-// HBM-bound.  One 32-thread group owns one (kv head, key block); each thread owns 4 channels and
+// HBM-bound.  One 64-thread CTA owns one (kv head, key block); each thread owns 2 channels and
 // sums the block's rows sequentially in fp32 — the reference's order (discovery.hpp:51-53) — then
 // multiplies by the fp32 reciprocal 1/len (discovery.hpp:55-56), so `pooled` is bit-identical to
 // the reference for identical inputs.  The same pass writes the bf16 hi/lo split of k̄ that the
@@ -12,81 +12,80 @@
 namespace fpb {
 
 template <bool kBf16>
-__global__ void __launch_bounds__(128) pool_keys_kernel(const void* __restrict__ K,
-                                                        float* __restrict__ pooled,
-                                                        __nv_bfloat16* __restrict__ split, int ZH,
-                                                        int L, int M, int last_len) {
-  const int group = blockIdx.x * 4 + (threadIdx.x >> 5);  // (zh, j) pair
-  if (group >= ZH * M) return;
-  const int zh = group / M, j = group % M;
-  const int c0 = (threadIdx.x & 31) * 4;
+__global__ void __launch_bounds__(64) pool_keys_kernel(const void* __restrict__ K,
+                                                       float* __restrict__ pooled,
+                                                       __nv_bfloat16* __restrict__ split, int ZH,
+                                                       int L, int M, int last_len) {
+  // one CTA of 64 threads per (zh, key block j); thread t owns channels 2t, 2t+1
+  const int zh = blockIdx.x / M, j = blockIdx.x % M;
+  const int c0 = threadIdx.x * 2;
   const int len = (j + 1 == M) ? last_len : kBlock;
   const size_t row0 = (size_t)zh * L + (size_t)j * kBlock;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  float s0 = 0.f, s1 = 0.f;
+  constexpr int U = 16;  // independent row loads in flight; the add chain stays sequential in r
   int r = 0;
-  constexpr int U = 8;
   for (; r + U <= len; r += U) {
-    float v[U][4];
+    float v[U][2];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const size_t off = (row0 + r + u) * kHeadDim + c0;
       if constexpr (kBf16) {
-        const uint2 raw = __ldg(reinterpret_cast<const uint2*>(
+        const uint32_t raw = __ldg(reinterpret_cast<const unsigned int*>(
             reinterpret_cast<const __nv_bfloat16*>(K) + off));
-        const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
-        const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
-        v[u][0] = __low2float(a); v[u][1] = __high2float(a);
-        v[u][2] = __low2float(b); v[u][3] = __high2float(b);
+        const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&raw);
+        v[u][0] = __low2float(a);
+        v[u][1] = __high2float(a);
       } else {
-        const float4 f = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(K) + off));
-        v[u][0] = f.x; v[u][1] = f.y; v[u][2] = f.z; v[u][3] = f.w;
+        const float2 f = __ldg(reinterpret_cast<const float2*>(reinterpret_cast<const float*>(K) + off));
+        v[u][0] = f.x;
+        v[u][1] = f.y;
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) {  // sequential accumulation order r, r+1, ...
-      s0 = __fadd_rn(s0, v[u][0]); s1 = __fadd_rn(s1, v[u][1]);
-      s2 = __fadd_rn(s2, v[u][2]); s3 = __fadd_rn(s3, v[u][3]);
+    for (int u = 0; u < U; ++u) {  // discovery.hpp:51-53: out[c] += row[c], r ascending
+      s0 = __fadd_rn(s0, v[u][0]);
+      s1 = __fadd_rn(s1, v[u][1]);
     }
   }
   for (; r < len; ++r) {
     const size_t off = (row0 + r) * kHeadDim + c0;
-    float v0, v1, v2, v3;
+    float v0, v1;
     if constexpr (kBf16) {
       const __nv_bfloat16* p = reinterpret_cast<const __nv_bfloat16*>(K) + off;
-      v0 = __bfloat162float(p[0]); v1 = __bfloat162float(p[1]);
-      v2 = __bfloat162float(p[2]); v3 = __bfloat162float(p[3]);
+      v0 = __bfloat162float(p[0]);
+      v1 = __bfloat162float(p[1]);
     } else {
       const float* p = reinterpret_cast<const float*>(K) + off;
-      v0 = p[0]; v1 = p[1]; v2 = p[2]; v3 = p[3];
+      v0 = p[0];
+      v1 = p[1];
     }
-    s0 = __fadd_rn(s0, v0); s1 = __fadd_rn(s1, v1); s2 = __fadd_rn(s2, v2); s3 = __fadd_rn(s3, v3);
+    s0 = __fadd_rn(s0, v0);
+    s1 = __fadd_rn(s1, v1);
   }
-  const float inv = __fdiv_rn(1.0f, (float)len);
-  const float o[4] = {__fmul_rn(s0, inv), __fmul_rn(s1, inv), __fmul_rn(s2, inv), __fmul_rn(s3, inv)};
+  const float inv = __fdiv_rn(1.0f, (float)len);  // discovery.hpp:55-56
+  const float o0 = __fmul_rn(s0, inv), o1 = __fmul_rn(s1, inv);
   const size_t dst = ((size_t)zh * M + j) * kHeadDim + c0;
-  if (pooled) *reinterpret_cast<float4*>(pooled + dst) = make_float4(o[0], o[1], o[2], o[3]);
+  if (pooled) *reinterpret_cast<float2*>(pooled + dst) = make_float2(o0, o1);
   if (split) {
-    __nv_bfloat16 hi[4], lo[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      hi[c] = __float2bfloat16_rn(o[c]);
-      lo[c] = __float2bfloat16_rn(__fsub_rn(o[c], __bfloat162float(hi[c])));
-    }
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(o0), h1 = __float2bfloat16_rn(o1);
+    const __nv_bfloat162 hi = __halves2bfloat162(h0, h1);
+    const __nv_bfloat162 lo = __halves2bfloat162(
+        __float2bfloat16_rn(__fsub_rn(o0, __bfloat162float(h0))),
+        __float2bfloat16_rn(__fsub_rn(o1, __bfloat162float(h1))));
     const size_t plane = (size_t)ZH * M * kHeadDim;
-    *reinterpret_cast<uint2*>(split + dst) = *reinterpret_cast<const uint2*>(hi);
-    *reinterpret_cast<uint2*>(split + plane + dst) = *reinterpret_cast<const uint2*>(lo);
+    *reinterpret_cast<__nv_bfloat162*>(split + dst) = hi;
+    *reinterpret_cast<__nv_bfloat162*>(split + plane + dst) = lo;
   }
 }
 
 cudaError_t launch_pool_keys(const Dims& D, bool bf16_in, const void* K, float* pooled,
                              __nv_bfloat16* kbar_split, cudaStream_t s) {
   const int ZH = D.Z * D.Hkv;
-  const int groups = ZH * D.M;
-  const dim3 grid((groups + 3) / 4);
+  const dim3 grid(ZH * D.M);
   if (bf16_in)
-    pool_keys_kernel<true><<<grid, 128, 0, s>>>(K, pooled, kbar_split, ZH, D.L, D.M, D.last_len);
+    pool_keys_kernel<true><<<grid, 64, 0, s>>>(K, pooled, kbar_split, ZH, D.L, D.M, D.last_len);
   else
-    pool_keys_kernel<false><<<grid, 128, 0, s>>>(K, pooled, kbar_split, ZH, D.L, D.M, D.last_len);
+    pool_keys_kernel<false><<<grid, 64, 0, s>>>(K, pooled, kbar_split, ZH, D.L, D.M, D.last_len);
   return cudaGetLastError();
 }
 

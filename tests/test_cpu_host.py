@@ -38,7 +38,7 @@ def test_abi_validation_without_gpu(lib):
     assert abs(p.alpha - 0.12) < 1e-7 and p.scale == 0.0
     n = ctypes.c_size_t(0)
     assert lib.fpb_workspace_bytes(ctypes.byref(p), _abi.FPB_BF16, ctypes.byref(n)) == 0
-    assert n.value == 2 * 4 * 256 * 128 * 2  # k̄ hi/lo split
+    assert n.value == 1024 + 2 * 4 * 256 * 128 * 2  # scheduler counter + k̄ hi/lo split
     bad = _abi.Problem()
     lib.fpb_problem_init(ctypes.byref(bad), 1, 6, 4, 100, 128)  # Hq % Hkv != 0
     assert lib.fpb_workspace_bytes(ctypes.byref(bad), 1, ctypes.byref(n)) == _abi.FPB_EVALIDATION

@@ -354,18 +354,23 @@ cudaError_t launch_ns(const Dims& D, const CUtensorMap& tm_q, const CUtensorMap&
 }  // namespace
 
 // Q / K: `splits` bf16 planes each ([hi][lo] for fp32 inputs); V: one bf16 plane.
+// bf16 (splits == 1) runs the persistent two-slot kernel (attention_fa.cu); the split-precision
+// fp32 path runs the one-tile kernel above.
 cudaError_t launch_attention(const Dims& D, int splits, const __nv_bfloat16* Q,
                              const __nv_bfloat16* K, const __nv_bfloat16* V, const int32_t* idx,
                              const int32_t* counts, bool out_bf16, void* out, float* lse,
-                             unsigned long long* visits, int32_t* plan_error, cudaStream_t s) {
+                             unsigned long long* visits, int32_t* plan_error, int* sched,
+                             cudaStream_t s) {
+  if (splits == 1)
+    return launch_attention_fa(D, Q, K, V, idx, counts, out_bf16, out, lse, visits, plan_error,
+                               sched, s);
   CUtensorMap tm_q, tm_k, tm_v;
   if (!make_tmap_rows128(&tm_q, Q, D.L, (uint64_t)splits * D.Z * D.Hq) ||
       !make_tmap_rows128(&tm_k, K, D.L, (uint64_t)splits * D.Z * D.Hkv) ||
       !make_tmap_rows128(&tm_v, V, D.L, (uint64_t)D.Z * D.Hkv))
     return cudaErrorInvalidValue;
   AttnParams prm{D, idx, counts, out, lse, visits, plan_error, out_bf16 ? 1 : 0};
-  return splits == 2 ? launch_ns<2>(D, tm_q, tm_k, tm_v, prm, s)
-                     : launch_ns<1>(D, tm_q, tm_k, tm_v, prm, s);
+  return launch_ns<2>(D, tm_q, tm_k, tm_v, prm, s);
 }
 
 }  // namespace fpb

@@ -1,0 +1,463 @@
+// attention_fa.cu — K4 block-sparse / K5 dense-causal FlashAttention prefill, bf16, persistent.
+//
+// Same semantics as attention.cu (block_sparse_attention, attention.hpp:38-132; dense_attention,
+// :135-174): index-driven jumps over the compacted plan row, causal mask only on the diagonal
+// block, listed j > i blocks attended in full, ragged last block, base-2 LSE, C = 0 -> NaN/-inf,
+// GQA by h / (Hq / Hkv).
+//
+// Persistent CTA per SM, FA4-style two-slot ping-pong: each CTA runs two independent work items
+// (z, h, query block i) at once, one per softmax warpgroup, so one slot's softmax (MUFU-bound)
+// overlaps the other slot's tensor-core work.
+//   TMEM (512 cols): S0 | S1 | O0 | O1; P (bf16) is written back over S and read by the PV MMA
+//   straight from TMEM (ts form).  Issue order per slot unit: PV(j-1) then QK(j) — in-order
+//   tcgen05 execution makes the S/P aliasing safe.
+//   SMEM: Q0, Q1 (32 KiB each) + a 4-tile K/V ring shared by both slots, filled by TMA in exactly
+//   the MMA consumption order (both warps run the same deterministic unit schedule).
+//
+// Warps: w0 scheduler + plan-row compaction + TMA producer; w1 MMA issuer; w2 TMEM allocator;
+// w3 idle; w4..w7 softmax/epilogue slot 0; w8..w11 softmax/epilogue slot 1.
+#include "fp_kernels.h"
+
+namespace fpb {
+
+using namespace ptx;
+
+namespace {
+
+constexpr int kThreads = 384;
+constexpr int kTile = kBlock * kHeadDim * 2;  // 32 KiB bf16 tile
+constexpr int kRing = 4;                      // shared K/V tile ring
+constexpr float kRescaleThreshold = 8.0f;     // lazy O rescale (log2 units)
+
+struct FaParams {
+  Dims D;
+  const int32_t* idx;  // nullptr -> dense causal
+  const int32_t* counts;
+  void* out;
+  float* lse;
+  unsigned long long* visits;
+  int32_t* plan_error;
+  int* sched;
+  int num_items;
+  int out_bf16;
+};
+
+struct SlotMeta {
+  int item;  // -1: no more work
+  int nblk;
+};
+
+struct FaSmem {
+  uint8_t q[2][kTile];
+  uint8_t ring[kRing][kTile];
+  uint64_t q_full[2], q_empty[2];
+  uint64_t kv_full[kRing], kv_empty[kRing];
+  uint64_t s_full[2], p_full[2], o_done[2], o_free[2];
+  uint64_t meta_full[2][2], meta_empty[2][2];
+  SlotMeta meta[2][2];
+  uint32_t tmem_base;
+  // followed by uint16_t list[2 slots][2 bufs][M] (sparse only)
+};
+
+__device__ __forceinline__ void decode(const Dims& D, int item, int& z, int& h, int& qi) {
+  h = item % D.Hq;
+  const int t = item / D.Hq;
+  qi = D.M - 1 - (t % D.M);  // heavy (long rows) first
+  z = t / D.M;
+}
+
+// Per-slot progress shared by the producer's and the MMA issuer's identical unit schedules.
+struct SlotState {
+  int t = 0;      // items taken by this slot (incl. empty ones and the final sentinel)
+  int j = 0;      // unit within the current item (0..nblk)
+  int nblk = 0;
+  int item = 0;
+  int qc = 0;     // items with nblk > 0 (Q loads / O lifetimes)
+  int bc = 0;     // blocks processed (P / S / O barrier phases)
+  bool active = true;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    fa_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+              const __grid_constant__ CUtensorMap tm_v, const FaParams prm) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  auto& s = *reinterpret_cast<FaSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                       ~uintptr_t(1023));
+  const Dims& D = prm.D;
+  const int N = D.M;
+  uint16_t* lists = reinterpret_cast<uint16_t*>(&s + 1);
+  auto list_of = [&](int slot, int p) { return lists + (size_t)(slot * 2 + p) * D.M; };
+  const bool dense = prm.idx == nullptr;
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&s.q_full[i]), 1);
+      mbar_init(smem_u32(&s.q_empty[i]), 1);
+      mbar_init(smem_u32(&s.s_full[i]), 1);
+      mbar_init(smem_u32(&s.p_full[i]), 4);
+      mbar_init(smem_u32(&s.o_done[i]), 1);
+      mbar_init(smem_u32(&s.o_free[i]), 4);
+      for (int p = 0; p < 2; ++p) {
+        mbar_init(smem_u32(&s.meta_full[i][p]), 1);
+        mbar_init(smem_u32(&s.meta_empty[i][p]), 4);
+      }
+    }
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(smem_u32(&s.kv_full[i]), 1);
+      mbar_init(smem_u32(&s.kv_empty[i]), 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(smem_u32(&s.tmem_base));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+  // 384 threads x 168 regs at launch; hand the control warpgroup's share to the softmax WGs
+  if (warp < 4) {
+  setmaxnreg_dec<72>();
+  if (warp == 0) {
+    // ===================== scheduler + plan-row compaction + TMA producer (whole warp)
+    const uint64_t pol_q = policy_evict_first();
+    const uint64_t pol_kv = policy_evict_last();
+    SlotState st[2];
+    int kvc = 0;  // tiles pushed through the ring
+    auto push = [&](const CUtensorMap* map, int row, int plane) {
+      const int r = kvc % kRing;
+      if (kvc >= kRing) mbar_wait(smem_u32(&s.kv_empty[r]), ((kvc / kRing) - 1) & 1);
+      if (lane == 0) {
+        const uint32_t fb = smem_u32(&s.kv_full[r]);
+        mbar_arrive_expect_tx(fb, kTile);
+        for (int a = 0; a < 2; ++a)
+          tma_load_3d_hint(smem_u32(s.ring[r]) + a * (kTile / 2), map, fb, a * 64, row, plane,
+                           pol_kv);
+      }
+      __syncwarp();
+      ++kvc;
+    };
+    while (st[0].active || st[1].active) {
+      for (int sl = 0; sl < 2; ++sl) {
+        SlotState& S = st[sl];
+        if (!S.active) continue;
+        const int p = S.t & 1;
+        if (S.j == 0) {
+          // ---- new item for this slot: fetch, compact the plan row into list[sl][p], publish
+          if (S.t >= 2) mbar_wait(smem_u32(&s.meta_empty[sl][p]), ((S.t >> 1) - 1) & 1);
+          int item = 0;
+          if (lane == 0) item = atomicAdd(prm.sched, 1);
+          item = __shfl_sync(0xffffffffu, item, 0);
+          if (item >= prm.num_items) item = -1;
+          int nblk = 0;
+          if (item >= 0) {
+            int z, h, qi;
+            decode(D, item, z, h, qi);
+            if (dense) {
+              nblk = qi + 1;
+            } else {
+              const int C = prm.counts[((size_t)z * D.M + qi) * D.Hq + h];
+              const size_t prow = ((size_t)z * D.M + qi) * (size_t)N;
+              uint16_t* lst = list_of(sl, p);
+              for (int s0 = 0; s0 < C; s0 += 32) {  // attention.hpp:76-81: range-check each slot
+                const int slot = s0 + lane;
+                int bid = -1;
+                if (slot < C) bid = prm.idx[(prow + slot) * D.Hq + h];
+                const bool ok = slot < C && bid >= 0 && bid < N;
+                if (slot < C && !ok && prm.plan_error) atomicExch(prm.plan_error, 1);
+                const unsigned bal = __ballot_sync(0xffffffffu, ok);
+                if (ok) lst[nblk + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)bid;
+                nblk += __popc(bal);
+              }
+              if (lane == 0 && prm.visits && nblk) atomicAdd(prm.visits, (unsigned long long)nblk);
+            }
+          }
+          if (lane == 0) {
+            s.meta[sl][p].item = item;
+            s.meta[sl][p].nblk = nblk;
+            mbar_arrive(smem_u32(&s.meta_full[sl][p]));
+          }
+          __syncwarp();
+          S.item = item;
+          S.nblk = nblk;
+          if (item < 0) {
+            S.active = false;
+            continue;
+          }
+          if (nblk == 0) {  // nothing to load; the softmax warps write NaN / -inf
+            ++S.t;
+            continue;
+          }
+          int z, h, qi;
+          decode(D, item, z, h, qi);
+          if (S.qc >= 1) mbar_wait(smem_u32(&s.q_empty[sl]), (S.qc - 1) & 1);
+          if (lane == 0) {
+            const uint32_t qb = smem_u32(&s.q_full[sl]);
+            mbar_arrive_expect_tx(qb, kTile);
+            for (int a = 0; a < 2; ++a)
+              tma_load_3d_hint(smem_u32(s.q[sl]) + a * (kTile / 2), &tm_q, qb, a * 64,
+                               qi * kBlock, z * D.Hq + h, pol_q);
+          }
+          __syncwarp();
+          ++S.qc;
+        }
+        // ---- one unit: V(j-1) then K(j), matching the MMA issue order PV(j-1), QK(j)
+        int z, h, qi;
+        decode(D, S.item, z, h, qi);
+        const int zkv = z * D.Hkv + h / D.group;
+        const uint16_t* lst = list_of(sl, p);
+        if (S.j >= 1) push(&tm_v, (dense ? S.j - 1 : (int)lst[S.j - 1]) * kBlock, zkv);
+        if (S.j < S.nblk) push(&tm_k, (dense ? S.j : (int)lst[S.j]) * kBlock, zkv);
+        if (++S.j == S.nblk + 1) {
+          S.j = 0;
+          ++S.t;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer: mirrors the producer's unit schedule
+    const bool leader = elect_one();
+    constexpr uint32_t idesc_qk = idesc_bf16_f32(128, 128, false, false);
+    constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, false, true);
+    SlotState st[2];
+    int kvc = 0;
+    while (st[0].active || st[1].active) {
+      for (int sl = 0; sl < 2; ++sl) {
+        SlotState& S = st[sl];
+        if (!S.active) continue;
+        const int p = S.t & 1;
+        const uint32_t s_tmem = tmem + sl * 128, o_tmem = tmem + 256 + sl * 128;
+        if (S.j == 0) {
+          mbar_wait(smem_u32(&s.meta_full[sl][p]), (S.t >> 1) & 1);
+          S.item = s.meta[sl][p].item;
+          S.nblk = s.meta[sl][p].nblk;
+          if (S.item < 0) {
+            S.active = false;
+            continue;
+          }
+          if (S.nblk == 0) {
+            ++S.t;
+            continue;
+          }
+          mbar_wait(smem_u32(&s.q_full[sl]), S.qc & 1);
+          ++S.qc;
+        }
+        if (S.j >= 1) {
+          // PV(j-1): O_sl (+)= P(j-1) [TMEM, aliasing S_sl] x V(j-1) [ring, MN-major]
+          const int m = S.j - 1;
+          if (m == 0 && S.qc >= 2) mbar_wait(smem_u32(&s.o_free[sl]), (S.qc - 2) & 1);
+          mbar_wait(smem_u32(&s.p_full[sl]), (S.bc - 1) & 1);
+          const int r = kvc % kRing;
+          mbar_wait(smem_u32(&s.kv_full[r]), (kvc / kRing) & 1);
+          tc_fence_after();
+          if (leader) {
+            const uint32_t vb = smem_u32(s.ring[r]);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              mma_bf16_ts(o_tmem, s_tmem + ks * 8, sdesc_sw128(vb + ks * 2048, kTile / 2, 1024),
+                          idesc_pv, (m > 0 || ks > 0) ? 1u : 0u);
+            mma_commit(smem_u32(&s.kv_empty[r]));
+            mma_commit(smem_u32(&s.o_done[sl]));
+          }
+          __syncwarp();
+          ++kvc;
+        }
+        if (S.j < S.nblk) {
+          // QK(j): S_sl = Q_sl K(j)^T
+          const int r = kvc % kRing;
+          mbar_wait(smem_u32(&s.kv_full[r]), (kvc / kRing) & 1);
+          tc_fence_after();
+          if (leader) {
+            const uint32_t qb = smem_u32(s.q[sl]), kb = smem_u32(s.ring[r]);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+              const uint32_t off = (ks >> 2) * (kTile / 2) + (ks & 3) * 32;
+              mma_bf16_ss(s_tmem, sdesc_sw128(qb + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024),
+                          idesc_qk, ks > 0 ? 1u : 0u);
+            }
+            mma_commit(smem_u32(&s.kv_empty[r]));
+            mma_commit(smem_u32(&s.s_full[sl]));
+            if (S.j == S.nblk - 1) mma_commit(smem_u32(&s.q_empty[sl]));
+          }
+          __syncwarp();
+          ++kvc;
+          ++S.bc;
+        }
+        if (++S.j == S.nblk + 1) {
+          S.j = 0;
+          ++S.t;
+        }
+      }
+    }
+  }
+  } else {
+    setmaxnreg_inc<216>();
+    // ===================== softmax + epilogue, one warpgroup per slot
+    const int sl = (warp - 4) >> 2;
+    const int r = ((warp - 4) & 3) * 32 + lane;  // query row == TMEM lane
+    const uint32_t lane_addr = static_cast<uint32_t>(((warp - 4) & 3) * 32) << 16;
+    const uint32_t s_addr = tmem + lane_addr + sl * 128;
+    const uint32_t o_addr = tmem + lane_addr + 256 + sl * 128;
+    int bc = 0, qc = 0;
+    for (int t = 0;; ++t) {
+      const int p = t & 1;
+      mbar_wait(smem_u32(&s.meta_full[sl][p]), (t >> 1) & 1);
+      const int item = s.meta[sl][p].item;
+      const int nblk = s.meta[sl][p].nblk;
+      if (item < 0) break;
+      const uint16_t* lst = list_of(sl, p);
+      int z, h, qi;
+      decode(D, item, z, h, qi);
+      const int rows = block_len(D, qi);
+      float m_used = -INFINITY, l = 0.f;
+      for (int n = 0; n < nblk; ++n, ++bc) {
+        const int kv = dense ? n : (int)lst[n];
+        const int cols = block_len(D, kv);
+        const int lim = (kv == qi) ? min(cols, r + 1) : cols;  // attention.hpp:85-91
+        const bool full = __all_sync(0xffffffffu, lim == kBlock);
+        mbar_wait(smem_u32(&s.s_full[sl]), bc & 1);
+        tc_fence_after();
+        uint32_t v[128];
+        tmem_ld32(s_addr + 0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+        tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+        tmem_ld32(s_addr + 64, *reinterpret_cast<uint32_t(*)[32]>(&v[64]));
+        tmem_ld32(s_addr + 96, *reinterpret_cast<uint32_t(*)[32]>(&v[96]));
+        tmem_ld_wait();
+        if (!full) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c >= lim) v[c] = __float_as_uint(-INFINITY);
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(v[c]));
+        const float m_new = fmaxf(m_used, mx * D.to_bits);
+        if (n == 0) {
+          m_used = m_new;
+        } else if (__any_sync(0xffffffffu, m_new > m_used + kRescaleThreshold)) {
+          // O must hold PV(n-1) before it is rescaled
+          mbar_wait(smem_u32(&s.o_done[sl]), (bc - 1) & 1);
+          tc_fence_after();
+          const float f = ex2_approx(m_used - m_new);
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            uint32_t o[32];
+            tmem_ld32(o_addr + cc * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * f);
+            tmem_st32(o_addr + cc * 32, o);
+          }
+          l *= f;
+          m_used = m_new;
+        }
+        const float neg_m = -m_used;
+        float bsum0 = 0.f, bsum1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 128; c += 2) {  // P packed in place: v[c/2] <- bf16x2(p_c, p_c+1)
+          const float p0 = ex2_approx(fmaf(__uint_as_float(v[c]), D.to_bits, neg_m));
+          const float p1 = ex2_approx(fmaf(__uint_as_float(v[c + 1]), D.to_bits, neg_m));
+          bsum0 += p0;
+          bsum1 += p1;
+          v[c >> 1] = pack_bf16x2(p0, p1);
+        }
+        l += bsum0 + bsum1;
+        tmem_st32(s_addr + 0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+        tmem_st32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&s.p_full[sl]));
+      }
+      // ---- epilogue (attention.hpp:119-126)
+      const size_t orow = ((size_t)z * D.Hq + h) * (size_t)D.L + (size_t)qi * kBlock + r;
+      if (nblk > 0) {
+        mbar_wait(smem_u32(&s.o_done[sl]), (bc - 1) & 1);
+        tc_fence_after();
+        const float inv = 1.0f / l;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t o[32];
+          tmem_ld32(o_addr + cc * 32, o);
+          tmem_ld_wait();
+          if (cc == 3) {  // O fully read: release the accumulator for the slot's next item
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&s.o_free[sl]));
+          }
+          if (r < rows) {
+            if (prm.out_bf16) {
+              uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(prm.out) +
+                                                    orow * kHeadDim + cc * 32);
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4)
+                dst[q4] = make_uint4(
+                    pack_bf16x2(__uint_as_float(o[8 * q4 + 0]) * inv, __uint_as_float(o[8 * q4 + 1]) * inv),
+                    pack_bf16x2(__uint_as_float(o[8 * q4 + 2]) * inv, __uint_as_float(o[8 * q4 + 3]) * inv),
+                    pack_bf16x2(__uint_as_float(o[8 * q4 + 4]) * inv, __uint_as_float(o[8 * q4 + 5]) * inv),
+                    pack_bf16x2(__uint_as_float(o[8 * q4 + 6]) * inv, __uint_as_float(o[8 * q4 + 7]) * inv));
+            } else {
+              float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(prm.out) +
+                                                      orow * kHeadDim + cc * 32);
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4)
+                dst[q4] = make_float4(__uint_as_float(o[4 * q4]) * inv,
+                                      __uint_as_float(o[4 * q4 + 1]) * inv,
+                                      __uint_as_float(o[4 * q4 + 2]) * inv,
+                                      __uint_as_float(o[4 * q4 + 3]) * inv);
+            }
+          }
+        }
+        if (r < rows) prm.lse[orow] = m_used + log2f(l);
+        ++qc;
+      } else if (r < rows) {  // C = 0: out = 0 * (1/0) = NaN, lse = -inf (attention.hpp:121-125)
+        const float nan = __int_as_float(0x7fc00000);
+        if (prm.out_bf16) {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(prm.out) + orow * kHeadDim);
+          const uint32_t pn = pack_bf16x2(nan, nan);
+          for (int q4 = 0; q4 < 16; ++q4) dst[q4] = make_uint4(pn, pn, pn, pn);
+        } else {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(prm.out) + orow * kHeadDim);
+          for (int q4 = 0; q4 < 32; ++q4) dst[q4] = make_float4(nan, nan, nan, nan);
+        }
+        prm.lse[orow] = -INFINITY;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&s.meta_empty[sl][p]));
+    }
+    (void)qc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+
+cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __nv_bfloat16* K,
+                                const __nv_bfloat16* V, const int32_t* idx, const int32_t* counts,
+                                bool out_bf16, void* out, float* lse, unsigned long long* visits,
+                                int32_t* plan_error, int* sched, cudaStream_t s) {
+  CUtensorMap tm_q, tm_k, tm_v;
+  if (!make_tmap_rows128(&tm_q, Q, D.L, (uint64_t)D.Z * D.Hq) ||
+      !make_tmap_rows128(&tm_k, K, D.L, (uint64_t)D.Z * D.Hkv) ||
+      !make_tmap_rows128(&tm_v, V, D.L, (uint64_t)D.Z * D.Hkv))
+    return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(sched, 0, sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  FaParams prm{D, idx, counts, out, lse, visits, plan_error, sched, D.Z * D.Hq * D.M,
+               out_bf16 ? 1 : 0};
+  const size_t smem = sizeof(FaSmem) + 1024 + (idx ? 4 * sizeof(uint16_t) * (size_t)D.M : 0);
+  e = cudaFuncSetAttribute(fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = prm.num_items < sms ? prm.num_items : sms;
+  fa_kernel<<<grid, kThreads, smem, s>>>(tm_q, tm_k, tm_v, prm);
+  return cudaGetLastError();
+}
+
+}  // namespace fpb

@@ -41,11 +41,16 @@ cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_
                             const __nv_bfloat16* kbar_split, const DiscoverOut& out, int* sched,
                             cudaStream_t s);
 
-// attention.cu — block-sparse (idx/counts) or dense-causal (idx == nullptr) tcgen05 attention.
+// attention.cu / attention_fa.cu — block-sparse (idx/counts) or dense-causal (idx == nullptr).
 cudaError_t launch_attention(const Dims& D, int splits, const __nv_bfloat16* Q,
-                             const __nv_bfloat16* K, const __nv_bfloat16* V, const int32_t* idx, const int32_t* counts,
-                             bool out_bf16, void* out, float* lse, unsigned long long* visits,
-                             int32_t* plan_error, cudaStream_t s);
+                             const __nv_bfloat16* K, const __nv_bfloat16* V, const int32_t* idx,
+                             const int32_t* counts, bool out_bf16, void* out, float* lse,
+                             unsigned long long* visits, int32_t* plan_error, int* sched,
+                             cudaStream_t s);
+cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __nv_bfloat16* K,
+                                const __nv_bfloat16* V, const int32_t* idx, const int32_t* counts,
+                                bool out_bf16, void* out, float* lse, unsigned long long* visits,
+                                int32_t* plan_error, int* sched, cudaStream_t s);
 
 // tensor maps (abi.cu)
 bool make_tmap_rows128(CUtensorMap* map, const void* base, uint64_t rows, uint64_t planes);

@@ -237,6 +237,16 @@ __device__ __forceinline__ uint32_t sw128_kmajor_offset(uint32_t row, uint32_t k
   return atom * rows * 128u + row * 128u + (chunk << 4) + (col_bytes & 15u);
 }
 
+// ---------------------------------------------------------------- register re-allocation
+template <uint32_t kRegs>
+__device__ __forceinline__ void setmaxnreg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+template <uint32_t kRegs>
+__device__ __forceinline__ void setmaxnreg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegs));
+}
+
 // ---------------------------------------------------------------- math
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;

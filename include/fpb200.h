@@ -117,6 +117,11 @@ int fpb_dense_attention(const fpb_problem* p, fpb_dtype dtype, const void* Q, co
 int fpb_full_causal_plan(const fpb_problem* p, int32_t* idx, int32_t* counts, void* stream);
 
 /* ---- Host-buffer entry points (copy in, run, copy out, synchronise) ----------------------- */
+int fpb_host_pool_keys(const fpb_problem* p, fpb_dtype dtype, const void* K, float* pooled);
+int fpb_host_approx_block_scores(const fpb_problem* p, fpb_dtype dtype, const void* Q,
+                                 const float* pooled, float* energy, float* local_max);
+int fpb_host_normalize_block_scores(const fpb_problem* p, const float* energy,
+                                    const float* local_max, float* score);
 int fpb_host_discover(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
                       float* energy, float* local_max, float* score);
 int fpb_host_max_threshold_mask(const fpb_problem* p, const float* score, uint8_t* mask,

@@ -20,6 +20,7 @@ EXPORTS = [
     "fpb_pool_keys", "fpb_approx_block_scores", "fpb_normalize_block_scores", "fpb_discover",
     "fpb_max_threshold_mask", "fpb_compress_indices", "fpb_discover_select", "fpb_visit_count",
     "fpb_block_sparse_attention", "fpb_dense_attention", "fpb_full_causal_plan",
+    "fpb_host_pool_keys", "fpb_host_approx_block_scores", "fpb_host_normalize_block_scores",
     "fpb_host_discover", "fpb_host_max_threshold_mask", "fpb_host_compress_indices",
     "fpb_host_block_sparse_attention", "fpb_host_dense_attention", "fpb_host_prefill",
 ]
@@ -69,6 +70,9 @@ def lib() -> C.CDLL:
             "fpb_dense_attention": (C.c_int, [P, C.c_int, p, p, p, C.c_int, p, p, p, C.c_size_t,
                                               p]),
             "fpb_full_causal_plan": (C.c_int, [P, p, p, p]),
+            "fpb_host_pool_keys": (C.c_int, [P, C.c_int, p, p]),
+            "fpb_host_approx_block_scores": (C.c_int, [P, C.c_int, p, p, p, p]),
+            "fpb_host_normalize_block_scores": (C.c_int, [P, p, p, p]),
             "fpb_host_discover": (C.c_int, [P, C.c_int, p, p, p, p, p]),
             "fpb_host_max_threshold_mask": (C.c_int, [P, p, p, u64p]),
             "fpb_host_compress_indices": (C.c_int, [P, p, p, p]),

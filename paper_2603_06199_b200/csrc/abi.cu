@@ -418,6 +418,74 @@ size_t dsz(fpb_dtype t) { return t == FPB_F32 ? 4 : 2; }
 
 extern "C" {
 
+int fpb_host_pool_keys(const fpb_problem* p, fpb_dtype dtype, const void* K, float* pooled) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc || (rc = check_dtype(dtype))) return rc;
+  if (!K || !pooled) return fail(FPB_EUSAGE, "null pointer");
+  const size_t kb = kv_elems(D) * dsz(dtype), pb = (size_t)D.Z * D.Hkv * D.M * kHeadDim * 4;
+  uint8_t* base;
+  cudaStream_t st;
+  if ((rc = arena_get(align_up(kb) + align_up(pb), &base, &st))) return rc;
+  Carve c{base};
+  void* dk = c.take<void>(kb);
+  float* dp = c.take<float>(pb);
+  FPB_CUDA(cudaMemcpyAsync(dk, K, kb, cudaMemcpyHostToDevice, st));
+  if ((rc = fpb_pool_keys(p, dtype, dk, dp, st))) return rc;
+  FPB_CUDA(cudaMemcpyAsync(pooled, dp, pb, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaStreamSynchronize(st));
+  return FPB_OK;
+}
+
+int fpb_host_approx_block_scores(const fpb_problem* p, fpb_dtype dtype, const void* Q,
+                                 const float* pooled, float* energy, float* local_max) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc || (rc = check_dtype(dtype))) return rc;
+  if (!Q || !pooled || !energy || !local_max) return fail(FPB_EUSAGE, "null pointer");
+  const size_t qb = q_elems(D) * dsz(dtype), pb = (size_t)D.Z * D.Hkv * D.M * kHeadDim * 4,
+               mb = map_elems(D) * 4, wsb = ws_discover(D, dtype);
+  uint8_t* base;
+  cudaStream_t st;
+  if ((rc = arena_get(align_up(qb) + align_up(pb) + 2 * align_up(mb) + align_up(wsb), &base, &st)))
+    return rc;
+  Carve c{base};
+  void* dq = c.take<void>(qb);
+  float* dp = c.take<float>(pb);
+  float* de = c.take<float>(mb);
+  float* dl = c.take<float>(mb);
+  void* ws = c.take<void>(wsb);
+  FPB_CUDA(cudaMemcpyAsync(dq, Q, qb, cudaMemcpyHostToDevice, st));
+  FPB_CUDA(cudaMemcpyAsync(dp, pooled, pb, cudaMemcpyHostToDevice, st));
+  if ((rc = fpb_approx_block_scores(p, dtype, dq, dp, de, dl, ws, wsb, st))) return rc;
+  FPB_CUDA(cudaMemcpyAsync(energy, de, mb, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaMemcpyAsync(local_max, dl, mb, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaStreamSynchronize(st));
+  return FPB_OK;
+}
+
+int fpb_host_normalize_block_scores(const fpb_problem* p, const float* energy,
+                                    const float* local_max, float* score) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc) return rc;
+  if (!energy || !local_max || !score) return fail(FPB_EUSAGE, "null pointer");
+  const size_t mb = map_elems(D) * 4;
+  uint8_t* base;
+  cudaStream_t st;
+  if ((rc = arena_get(3 * align_up(mb), &base, &st))) return rc;
+  Carve c{base};
+  float* de = c.take<float>(mb);
+  float* dl = c.take<float>(mb);
+  float* ds = c.take<float>(mb);
+  FPB_CUDA(cudaMemcpyAsync(de, energy, mb, cudaMemcpyHostToDevice, st));
+  FPB_CUDA(cudaMemcpyAsync(dl, local_max, mb, cudaMemcpyHostToDevice, st));
+  if ((rc = fpb_normalize_block_scores(p, de, dl, ds, st))) return rc;
+  FPB_CUDA(cudaMemcpyAsync(score, ds, mb, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaStreamSynchronize(st));
+  return FPB_OK;
+}
+
 int fpb_host_discover(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
                       float* energy, float* local_max, float* score) {
   Dims D;

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfpb200.so")
+LIB_PATH = os.environ.get("FPB200_LIB") or os.path.join(HERE, "libfpb200.so")
 
 FPB_OK, FPB_EUSAGE, FPB_EVALIDATION, FPB_EFORMAT, FPB_ECUDA = 0, 1, 2, 3, 4
 FPB_F32, FPB_BF16 = 0, 1

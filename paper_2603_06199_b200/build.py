@@ -29,19 +29,21 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    if not force and out == LIB and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, f) for f in SOURCES]]
-    out = subprocess.run(cmd, capture_output=True, text=True)
-    if out.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + out.stdout + out.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
-        f.write(out.stderr)
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", out + ".tmp",
+           *[os.path.join(CSRC, f) for f in SOURCES]]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
+    os.replace(out + ".tmp", out)
+    if out == LIB:
+        with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
+            f.write(res.stderr)
     if verbose:
-        print(out.stderr)
-    return LIB
+        print(res.stderr)
+    return out
 
 
 if __name__ == "__main__":

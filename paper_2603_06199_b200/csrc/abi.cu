@@ -14,6 +14,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/fpb200.h"
 #include "fp_kernels.h"
@@ -380,9 +381,12 @@ struct Arena {
   void* ptr = nullptr;
   size_t cap = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t s_in = nullptr, s_out = nullptr;  // copy streams of the pipelined prefill
   ~Arena() {
     if (ptr) cudaFree(ptr);
     if (stream) cudaStreamDestroy(stream);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
   }
 };
 thread_local Arena g_arena;
@@ -638,48 +642,114 @@ int fpb_host_dense_attention(const fpb_problem* p, fpb_dtype dtype, const void* 
 int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
                      const void* V, fpb_dtype out_dtype, void* out, float* lse, int32_t* idx,
                      int32_t* counts, unsigned long long* visits) {
+  // Pipelined over chunks of Q heads (each inside one KV group): H2D of chunk c+1, the kernels of
+  // chunk c and the D2H of chunk c-1 run concurrently on three streams (PCIe is full duplex).
   Dims D;
   int rc = resolve(p, &D);
   if (rc || (rc = check_dtype(dtype)) || (rc = check_dtype(out_dtype))) return rc;
   if (!Q || !K || !V || !out || !lse) return fail(FPB_EUSAGE, "null pointer");
-  const size_t qb = q_elems(D) * dsz(dtype), kb = kv_elems(D) * dsz(dtype),
-               ob = q_elems(D) * dsz(out_dtype), lb = (size_t)D.Z * D.Hq * D.L * 4,
-               ib = map_elems(D) * 4, cb = (size_t)D.Z * D.M * D.Hq * 4;
-  const size_t wsd = ws_discover(D, dtype), wsa = ws_attention(D, dtype);
+  const int group = D.Hq / D.Hkv;
+  int cq = group;  // Q heads per chunk: at least 8 chunks when the problem allows it
+  while (cq % 2 == 0 && (int64_t)D.Z * D.Hq / cq < 8) cq /= 2;
+  const int chunks_per_z = D.Hq / cq, nch = D.Z * chunks_per_z;
+  const size_t es = dsz(dtype), eo = dsz(out_dtype), Ld = (size_t)D.L * kHeadDim;
+  const size_t qb = q_elems(D) * es, kb = kv_elems(D) * es, ob = q_elems(D) * eo,
+               lb = (size_t)D.Z * D.Hq * D.L * 4;
+  fpb_problem sub = *p;
+  sub.Z = 1;
+  sub.Hq = cq;
+  sub.Hkv = 1;
+  Dims Ds;
+  if ((rc = resolve(&sub, &Ds))) return rc;
+  const size_t sib = map_elems(Ds) * 4, scb = (size_t)Ds.M * cq * 4;
+  const size_t wsd = ws_discover(Ds, dtype), wsa = ws_attention(Ds, dtype);
   const size_t wsb = wsd > wsa ? wsd : wsa;
   const size_t need = align_up(qb) + 2 * align_up(kb) + align_up(ob) + align_up(lb) +
-                      align_up(ib) + align_up(cb) + align_up(wsb) + 2048;
+                      nch * (align_up(sib) + align_up(scb)) + align_up(8 * nch) + align_up(wsb);
   uint8_t* base;
   cudaStream_t st;
   if ((rc = arena_get(need, &base, &st))) return rc;
+  if (!g_arena.s_in) FPB_CUDA(cudaStreamCreateWithFlags(&g_arena.s_in, cudaStreamNonBlocking));
+  if (!g_arena.s_out) FPB_CUDA(cudaStreamCreateWithFlags(&g_arena.s_out, cudaStreamNonBlocking));
+  cudaStream_t s_in = g_arena.s_in, s_out = g_arena.s_out;
   Carve c{base};
-  void* dq = c.take<void>(qb);
-  void* dk = c.take<void>(kb);
-  void* dv = c.take<void>(kb);
-  void* dout = c.take<void>(ob);
+  uint8_t* dq = c.take<uint8_t>(qb);
+  uint8_t* dk = c.take<uint8_t>(kb);
+  uint8_t* dv = c.take<uint8_t>(kb);
+  uint8_t* dout = c.take<uint8_t>(ob);
   float* dl = c.take<float>(lb);
-  int32_t* di = c.take<int32_t>(ib);
-  int32_t* dc = c.take<int32_t>(cb);
-  unsigned long long* dvis = c.take<unsigned long long>(8);
+  unsigned long long* dvis = c.take<unsigned long long>(8 * nch);
   void* ws = c.take<void>(wsb);
-  FPB_CUDA(cudaMemcpyAsync(dq, Q, qb, cudaMemcpyHostToDevice, st));
-  FPB_CUDA(cudaMemcpyAsync(dk, K, kb, cudaMemcpyHostToDevice, st));
-  FPB_CUDA(cudaMemcpyAsync(dv, V, kb, cudaMemcpyHostToDevice, st));
-  FPB_CUDA(cudaMemsetAsync(dvis, 0, 8, st));
-  if ((rc = fpb_discover_select(p, dtype, dq, dk, nullptr, nullptr, nullptr, nullptr, di, dc, ws,
-                                wsb, st)))
-    return rc;
-  if ((rc = fpb_block_sparse_attention(p, dtype, dq, dk, dv, di, dc, out_dtype, dout, dl, dvis,
-                                       nullptr, ws, wsb, st)))
-    return rc;
-  FPB_CUDA(cudaMemcpyAsync(out, dout, ob, cudaMemcpyDeviceToHost, st));
-  FPB_CUDA(cudaMemcpyAsync(lse, dl, lb, cudaMemcpyDeviceToHost, st));
-  if (idx) FPB_CUDA(cudaMemcpyAsync(idx, di, ib, cudaMemcpyDeviceToHost, st));
-  if (counts) FPB_CUDA(cudaMemcpyAsync(counts, dc, cb, cudaMemcpyDeviceToHost, st));
-  unsigned long long vis = 0;
-  FPB_CUDA(cudaMemcpyAsync(&vis, dvis, 8, cudaMemcpyDeviceToHost, st));
+  std::vector<int32_t*> di(nch), dc(nch);
+  for (int i = 0; i < nch; ++i) {
+    di[i] = c.take<int32_t>(sib);
+    dc[i] = c.take<int32_t>(scb);
+  }
+  std::vector<cudaEvent_t> ev_in(nch), ev_done(nch);
+  for (int i = 0; i < nch; ++i) {
+    FPB_CUDA(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
+    FPB_CUDA(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming));
+  }
+  FPB_CUDA(cudaMemsetAsync(dvis, 0, 8 * nch, st));
+  const uint8_t* hq = static_cast<const uint8_t*>(Q);
+  const uint8_t* hk = static_cast<const uint8_t*>(K);
+  const uint8_t* hv = static_cast<const uint8_t*>(V);
+  for (int i = 0; i < nch; ++i) {  // H2D: K/V of a group with its first chunk, then the Q slice
+    const int z = i / chunks_per_z, q0 = (i % chunks_per_z) * cq, kv = q0 / group;
+    if (q0 % group == 0) {
+      const size_t off = ((size_t)z * D.Hkv + kv) * Ld * es;
+      FPB_CUDA(cudaMemcpyAsync(dk + off, hk + off, Ld * es, cudaMemcpyHostToDevice, s_in));
+      FPB_CUDA(cudaMemcpyAsync(dv + off, hv + off, Ld * es, cudaMemcpyHostToDevice, s_in));
+    }
+    const size_t off = ((size_t)z * D.Hq + q0) * Ld * es;
+    FPB_CUDA(cudaMemcpyAsync(dq + off, hq + off, cq * Ld * es, cudaMemcpyHostToDevice, s_in));
+    FPB_CUDA(cudaEventRecord(ev_in[i], s_in));
+  }
+  for (int i = 0; i < nch; ++i) {  // kernels of each chunk on the compute stream
+    const int z = i / chunks_per_z, q0 = (i % chunks_per_z) * cq, kv = q0 / group;
+    FPB_CUDA(cudaStreamWaitEvent(st, ev_in[i], 0));
+    const uint8_t* q = dq + ((size_t)z * D.Hq + q0) * Ld * es;
+    const uint8_t* k = dk + ((size_t)z * D.Hkv + kv) * Ld * es;
+    const uint8_t* v = dv + ((size_t)z * D.Hkv + kv) * Ld * es;
+    uint8_t* o = dout + ((size_t)z * D.Hq + q0) * Ld * eo;
+    float* l = dl + ((size_t)z * D.Hq + q0) * D.L;
+    if ((rc = fpb_discover_select(&sub, dtype, q, k, nullptr, nullptr, nullptr, nullptr, di[i],
+                                  dc[i], ws, wsb, st)))
+      return rc;
+    if ((rc = fpb_block_sparse_attention(&sub, dtype, q, k, v, di[i], dc[i], out_dtype, o, l,
+                                         dvis + i, nullptr, ws, wsb, st)))
+      return rc;
+    FPB_CUDA(cudaEventRecord(ev_done[i], st));
+  }
+  uint8_t* ho = static_cast<uint8_t*>(out);
+  for (int i = 0; i < nch; ++i) {  // D2H of each finished chunk
+    const int z = i / chunks_per_z, q0 = (i % chunks_per_z) * cq;
+    FPB_CUDA(cudaStreamWaitEvent(s_out, ev_done[i], 0));
+    const size_t oo = ((size_t)z * D.Hq + q0) * Ld * eo;
+    FPB_CUDA(cudaMemcpyAsync(ho + oo, dout + oo, cq * Ld * eo, cudaMemcpyDeviceToHost, s_out));
+    const size_t lo = ((size_t)z * D.Hq + q0) * D.L;
+    FPB_CUDA(cudaMemcpyAsync(lse + lo, dl + lo, (size_t)cq * D.L * 4, cudaMemcpyDeviceToHost,
+                             s_out));
+    // plans are head-last: scatter the chunk's heads into the caller's Z x M x N x Hq layout
+    if (idx)
+      FPB_CUDA(cudaMemcpy2DAsync(idx + (size_t)z * D.M * D.M * D.Hq + q0, (size_t)D.Hq * 4, di[i],
+                                 (size_t)cq * 4, (size_t)cq * 4, (size_t)D.M * D.M,
+                                 cudaMemcpyDeviceToHost, s_out));
+    if (counts)
+      FPB_CUDA(cudaMemcpy2DAsync(counts + (size_t)z * D.M * D.Hq + q0, (size_t)D.Hq * 4, dc[i],
+                                 (size_t)cq * 4, (size_t)cq * 4, (size_t)D.M,
+                                 cudaMemcpyDeviceToHost, s_out));
+  }
+  std::vector<unsigned long long> vis(nch, 0);
   FPB_CUDA(cudaStreamSynchronize(st));
-  if (visits) *visits += vis;
+  FPB_CUDA(cudaMemcpyAsync(vis.data(), dvis, 8 * nch, cudaMemcpyDeviceToHost, s_out));
+  FPB_CUDA(cudaStreamSynchronize(s_out));
+  for (int i = 0; i < nch; ++i) {
+    cudaEventDestroy(ev_in[i]);
+    cudaEventDestroy(ev_done[i]);
+  }
+  if (visits)
+    for (auto x : vis) *visits += x;
   return FPB_OK;
 }
 

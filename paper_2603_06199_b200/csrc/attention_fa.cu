@@ -14,8 +14,10 @@
 //   SMEM: Q0, Q1 (32 KiB each) + a 4-tile K/V ring shared by both slots, filled by TMA in exactly
 //   the MMA consumption order (both warps run the same deterministic unit schedule).
 //
-// Warps: w0 scheduler + plan-row compaction + TMA producer; w1 MMA issuer; w2 TMEM allocator;
-// w3 idle; w4..w7 softmax/epilogue slot 0; w8..w11 softmax/epilogue slot 1.
+// Warps: w0 TMA producer; w1 MMA issuer; w2 TMEM allocator; w3 scheduler (dynamic work counter,
+// plan-row fetch + range check + compaction, two items ahead per slot); w4..w7 softmax/epilogue
+// slot 0; w8..w11 softmax/epilogue slot 1.  PV(j) is issued in two K-halves, each released as
+// soon as that half of P is in TMEM.
 #include "fp_kernels.h"
 
 namespace fpb {
@@ -28,6 +30,9 @@ constexpr int kThreads = 384;
 constexpr int kTile = kBlock * kHeadDim * 2;  // 32 KiB bf16 tile
 constexpr int kRing = 4;                      // shared K/V tile ring
 constexpr float kRescaleThreshold = 8.0f;     // lazy O rescale (log2 units)
+#ifndef FPB_POLY_MASK
+#define FPB_POLY_MASK 0  // pairs p with (p & 3) in this bit mask use exp2_poly2 (FMA pipe)
+#endif
 
 struct FaParams {
   Dims D;
@@ -52,7 +57,7 @@ struct FaSmem {
   uint8_t ring[kRing][kTile];
   uint64_t q_full[2], q_empty[2];
   uint64_t kv_full[kRing], kv_empty[kRing];
-  uint64_t s_full[2], p_full[2], o_done[2], o_free[2];
+  uint64_t s_full[2], p_half[2], p_full[2], o_done[2], o_free[2];
   uint64_t meta_full[2][2], meta_empty[2][2];
   SlotMeta meta[2][2];
   uint32_t tmem_base;
@@ -98,6 +103,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&s.q_full[i]), 1);
       mbar_init(smem_u32(&s.q_empty[i]), 1);
       mbar_init(smem_u32(&s.s_full[i]), 1);
+      mbar_init(smem_u32(&s.p_half[i]), 4);
       mbar_init(smem_u32(&s.p_full[i]), 4);
       mbar_init(smem_u32(&s.o_done[i]), 1);
       mbar_init(smem_u32(&s.o_free[i]), 4);
@@ -120,8 +126,60 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 384 threads x 168 regs at launch; hand the control warpgroup's share to the softmax WGs
   if (warp < 4) {
   setmaxnreg_dec<72>();
-  if (warp == 0) {
-    // ===================== scheduler + plan-row compaction + TMA producer (whole warp)
+  if (warp == 3) {
+    // ===================== scheduler: fetch items, compact plan rows, publish per-slot metas
+    // (runs up to two items ahead per slot so plan-row loads never stall the TMA producer)
+    int t[2] = {0, 0};
+    bool done[2] = {false, false};
+    while (!done[0] || !done[1]) {
+      for (int sl = 0; sl < 2; ++sl) {
+        if (done[sl]) continue;
+        const int p = t[sl] & 1;
+        if (t[sl] >= 2) {
+          const bool ready = mbar_try_wait(smem_u32(&s.meta_empty[sl][p]), ((t[sl] >> 1) - 1) & 1);
+          if (!__shfl_sync(0xffffffffu, ready, 0)) continue;
+        }
+        __syncwarp();
+        int item = 0;
+        if (lane == 0) item = atomicAdd(prm.sched, 1);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= prm.num_items) item = -1;
+        int nblk = 0;
+        if (item >= 0) {
+          int z, h, qi;
+          decode(D, item, z, h, qi);
+          if (dense) {
+            nblk = qi + 1;
+          } else {
+            const int C = prm.counts[((size_t)z * D.M + qi) * D.Hq + h];
+            const size_t prow = ((size_t)z * D.M + qi) * (size_t)N;
+            uint16_t* lst = list_of(sl, p);
+            for (int s0 = 0; s0 < C; s0 += 32) {  // attention.hpp:76-81: range-check each slot
+              const int slot = s0 + lane;
+              int bid = -1;
+              if (slot < C) bid = prm.idx[(prow + slot) * D.Hq + h];
+              const bool ok = slot < C && bid >= 0 && bid < N;
+              if (slot < C && !ok && prm.plan_error) atomicExch(prm.plan_error, 1);
+              const unsigned bal = __ballot_sync(0xffffffffu, ok);
+              if (ok) lst[nblk + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)bid;
+              nblk += __popc(bal);
+            }
+            if (lane == 0 && prm.visits && nblk) atomicAdd(prm.visits, (unsigned long long)nblk);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          s.meta[sl][p].item = item;
+          s.meta[sl][p].nblk = nblk;
+          mbar_arrive(smem_u32(&s.meta_full[sl][p]));
+        }
+        __syncwarp();
+        ++t[sl];
+        if (item < 0) done[sl] = true;
+      }
+    }
+  } else if (warp == 0) {
+    // ===================== TMA producer (whole warp; lane 0 issues)
     const uint64_t pol_q = policy_evict_first();
     const uint64_t pol_kv = policy_evict_last();
     SlotState st[2];
@@ -145,53 +203,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!S.active) continue;
         const int p = S.t & 1;
         if (S.j == 0) {
-          // ---- new item for this slot: fetch, compact the plan row into list[sl][p], publish
-          if (S.t >= 2) mbar_wait(smem_u32(&s.meta_empty[sl][p]), ((S.t >> 1) - 1) & 1);
-          int item = 0;
-          if (lane == 0) item = atomicAdd(prm.sched, 1);
-          item = __shfl_sync(0xffffffffu, item, 0);
-          if (item >= prm.num_items) item = -1;
-          int nblk = 0;
-          if (item >= 0) {
-            int z, h, qi;
-            decode(D, item, z, h, qi);
-            if (dense) {
-              nblk = qi + 1;
-            } else {
-              const int C = prm.counts[((size_t)z * D.M + qi) * D.Hq + h];
-              const size_t prow = ((size_t)z * D.M + qi) * (size_t)N;
-              uint16_t* lst = list_of(sl, p);
-              for (int s0 = 0; s0 < C; s0 += 32) {  // attention.hpp:76-81: range-check each slot
-                const int slot = s0 + lane;
-                int bid = -1;
-                if (slot < C) bid = prm.idx[(prow + slot) * D.Hq + h];
-                const bool ok = slot < C && bid >= 0 && bid < N;
-                if (slot < C && !ok && prm.plan_error) atomicExch(prm.plan_error, 1);
-                const unsigned bal = __ballot_sync(0xffffffffu, ok);
-                if (ok) lst[nblk + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)bid;
-                nblk += __popc(bal);
-              }
-              if (lane == 0 && prm.visits && nblk) atomicAdd(prm.visits, (unsigned long long)nblk);
-            }
-          }
-          if (lane == 0) {
-            s.meta[sl][p].item = item;
-            s.meta[sl][p].nblk = nblk;
-            mbar_arrive(smem_u32(&s.meta_full[sl][p]));
-          }
-          __syncwarp();
-          S.item = item;
-          S.nblk = nblk;
-          if (item < 0) {
+          mbar_wait(smem_u32(&s.meta_full[sl][p]), (S.t >> 1) & 1);
+          S.item = s.meta[sl][p].item;
+          S.nblk = s.meta[sl][p].nblk;
+          if (S.item < 0) {
             S.active = false;
             continue;
           }
-          if (nblk == 0) {  // nothing to load; the softmax warps write NaN / -inf
+          if (S.nblk == 0) {  // nothing to load; the softmax warps write NaN / -inf
             ++S.t;
             continue;
           }
           int z, h, qi;
-          decode(D, item, z, h, qi);
+          decode(D, S.item, z, h, qi);
           if (S.qc >= 1) mbar_wait(smem_u32(&s.q_empty[sl]), (S.qc - 1) & 1);
           if (lane == 0) {
             const uint32_t qb = smem_u32(&s.q_full[sl]);
@@ -248,16 +272,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           // PV(j-1): O_sl (+)= P(j-1) [TMEM, aliasing S_sl] x V(j-1) [ring, MN-major]
           const int m = S.j - 1;
           if (m == 0 && S.qc >= 2) mbar_wait(smem_u32(&s.o_free[sl]), (S.qc - 2) & 1);
-          mbar_wait(smem_u32(&s.p_full[sl]), (S.bc - 1) & 1);
           const int r = kvc % kRing;
           mbar_wait(smem_u32(&s.kv_full[r]), (kvc / kRing) & 1);
-          tc_fence_after();
-          if (leader) {
-            const uint32_t vb = smem_u32(s.ring[r]);
+          const uint32_t vb = smem_u32(s.ring[r]);
+          // keys 0..63 as soon as the first half of P is in TMEM, keys 64..127 after the rest
+          for (int half = 0; half < 2; ++half) {
+            mbar_wait(smem_u32(half ? &s.p_full[sl] : &s.p_half[sl]), (S.bc - 1) & 1);
+            tc_fence_after();
+            if (leader) {
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks)
-              mma_bf16_ts(o_tmem, s_tmem + ks * 8, sdesc_sw128(vb + ks * 2048, kTile / 2, 1024),
-                          idesc_pv, (m > 0 || ks > 0) ? 1u : 0u);
+              for (int k4 = 0; k4 < 4; ++k4) {
+                const int ks = half * 4 + k4;
+                mma_bf16_ts(o_tmem, s_tmem + ks * 8, sdesc_sw128(vb + ks * 2048, kTile / 2, 1024),
+                            idesc_pv, (m > 0 || ks > 0) ? 1u : 0u);
+              }
+            }
+            __syncwarp();
+          }
+          if (leader) {
             mma_commit(smem_u32(&s.kv_empty[r]));
             mma_commit(smem_u32(&s.o_done[sl]));
           }
@@ -330,9 +362,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < 128; ++c)
             if (c >= lim) v[c] = __float_as_uint(-INFINITY);
         }
-        float mx = -INFINITY;
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(v[c]));
+        for (int c = 0; c < 128; c += 8) {  // 4 independent 3-input max chains
+          mx0 = fmaxf(mx0, fmaxf(__uint_as_float(v[c + 0]), __uint_as_float(v[c + 1])));
+          mx1 = fmaxf(mx1, fmaxf(__uint_as_float(v[c + 2]), __uint_as_float(v[c + 3])));
+          mx2 = fmaxf(mx2, fmaxf(__uint_as_float(v[c + 4]), __uint_as_float(v[c + 5])));
+          mx3 = fmaxf(mx3, fmaxf(__uint_as_float(v[c + 6]), __uint_as_float(v[c + 7])));
+        }
+        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
         const float m_new = fmaxf(m_used, mx * D.to_bits);
         if (n == 0) {
           m_used = m_new;
@@ -353,23 +391,44 @@ __global__ void __launch_bounds__(kThreads, 1)
           l *= f;
           m_used = m_new;
         }
-        const float neg_m = -m_used;
-        float bsum0 = 0.f, bsum1 = 0.f;
+        const float neg_m = -m_used, sc = D.to_bits;
+        float bs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int c = 0; c < 128; c += 2) {  // P packed in place: v[c/2] <- bf16x2(p_c, p_c+1)
-          const float p0 = ex2_approx(fmaf(__uint_as_float(v[c]), D.to_bits, neg_m));
-          const float p1 = ex2_approx(fmaf(__uint_as_float(v[c + 1]), D.to_bits, neg_m));
-          bsum0 += p0;
-          bsum1 += p1;
-          v[c >> 1] = pack_bf16x2(p0, p1);
+        for (int half = 0; half < 2; ++half) {
+          // P packed in place: v[c/2] <- bf16x2(p_c, p_c+1); columns [64 half, 64 half + 64)
+          if (full) {
+            // MUFU-bound: every other pair of exponentials goes to the FMA pipe (exp2_poly2)
+#pragma unroll
+            for (int c = half * 64; c < half * 64 + 64; c += 2) {
+              float x0, x1, p0, p1;
+              ffma2(x0, x1, __uint_as_float(v[c]), __uint_as_float(v[c + 1]), sc, sc, neg_m, neg_m);
+              if ((FPB_POLY_MASK >> ((c >> 1) & 3)) & 1) {
+                exp2_poly2(x0, x1, p0, p1);
+              } else {
+                p0 = ex2_approx(x0);
+                p1 = ex2_approx(x1);
+              }
+              const int a = ((c >> 1) & 3) * 2;
+              fadd2(bs[a], bs[a + 1], bs[a], bs[a + 1], p0, p1);
+              v[c >> 1] = pack_bf16x2(p0, p1);
+            }
+          } else {
+#pragma unroll
+            for (int c = half * 64; c < half * 64 + 64; c += 2) {
+              const float p0 = ex2_approx(fmaf(__uint_as_float(v[c]), sc, neg_m));
+              const float p1 = ex2_approx(fmaf(__uint_as_float(v[c + 1]), sc, neg_m));
+              const int a = ((c >> 1) & 3) * 2;
+              fadd2(bs[a], bs[a + 1], bs[a], bs[a + 1], p0, p1);
+              v[c >> 1] = pack_bf16x2(p0, p1);
+            }
+          }
+          tmem_st32(s_addr + half * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[half * 32]));
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(half ? &s.p_full[sl] : &s.p_half[sl]));
         }
-        l += bsum0 + bsum1;
-        tmem_st32(s_addr + 0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-        tmem_st32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&s.p_full[sl]));
+        l += ((bs[0] + bs[1]) + (bs[2] + bs[3])) + ((bs[4] + bs[5]) + (bs[6] + bs[7]));
       }
       // ---- epilogue (attention.hpp:119-126)
       const size_t orow = ((size_t)z * D.Hq + h) * (size_t)D.L + (size_t)qi * kBlock + r;

@@ -15,12 +15,13 @@
 // accumulating MMAs); bf16 Q is exact.  fp32 Q (the C1 config) is split too (3 MMAs: hh, hl, lh).
 // Naively rounding k̄ to bf16 flips mask bits (SURVEY §7 hard part 1).
 //
-// Warp roles (256 threads, persistent):
+// Warp roles (384 threads, persistent):
 //   w0  scheduler + TMA producer: item ring, Q tiles (double-buffered), k̄ chunk ring
-//   w1  MMA issuer (single thread), TMEM accumulators double-buffered across chunks/items
-//   w2  TMEM allocator;  w3 idle
-//   w4..w7 epilogue: TMEM -> (m, S) per pair, then row normalisation, threshold, compaction for
-//          the item while the MMA warp already works on the next one.
+//   w1  MMA issuer (single thread); TMEM accumulators double-buffered per epilogue warpgroup
+//   w2  TMEM allocator (512 cols);  w3 idle
+//   w4..w7, w8..w11  two epilogue warpgroups, items alternating: TMEM -> (m, S) per pair, then
+//          row normalisation, threshold and compaction for the item while the MMA warp and the
+//          other warpgroup already work on the next ones.
 #include "fp_kernels.h"
 
 namespace fpb {
@@ -29,12 +30,12 @@ using namespace ptx;
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kEpiThreads = 128;
+constexpr int kThreads = 384;
+constexpr int kEpiThreads = 128;               // per epilogue warpgroup (two of them)
 constexpr int kTile = kBlock * kHeadDim * 2;  // one bf16 128x128 operand tile: 32 KiB
 constexpr int kStages = 2;                    // k̄ chunk ring (hi + lo per stage)
 constexpr int kItemRing = 4;
-constexpr uint32_t kEpiBar = 1;               // named barrier of the 128 epilogue threads
+constexpr uint32_t kEpiBar = 1;               // named barriers 1, 2: the two epilogue warpgroups
 
 struct DiscParams {
   Dims D;
@@ -50,13 +51,13 @@ struct DiscSmem {
   uint8_t kb[kStages][2][kTile];
   uint64_t q_full[kQBuf], q_empty[kQBuf];
   uint64_t kb_full[kStages], kb_empty[kStages];
-  uint64_t d_full[2], d_empty[2];
+  uint64_t d_full[4], d_empty[4];  // TMEM accumulators: 2 per epilogue warpgroup
   uint64_t it_full[kItemRing], it_empty[kItemRing];
   int items[kItemRing];
   uint32_t tmem_base;
-  float red[8];
-  int ired[8];
-  // followed by float m_s[M], S_s[M] (dynamic)
+  float red[2][8];
+  int ired[2][8];
+  // followed by float m_s[M], S_s[M] per epilogue warpgroup (dynamic)
 };
 
 __device__ __forceinline__ void decode_item(const Dims& D, int item, int& z, int& h, int& I) {
@@ -67,26 +68,26 @@ __device__ __forceinline__ void decode_item(const Dims& D, int item, int& z, int
 }
 
 // Reductions over the 128 epilogue threads (named barrier kEpiBar).
-__device__ __forceinline__ float epi_max(float v, float* red) {
+__device__ __forceinline__ float epi_max(float v, float* red, uint32_t bar) {
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  named_bar_sync(kEpiBar, kEpiThreads);
-  if (lane_id() == 0) red[warp_id() - 4] = v;
-  named_bar_sync(kEpiBar, kEpiThreads);
+  named_bar_sync(bar, kEpiThreads);
+  if (lane_id() == 0) red[warp_id() & 3] = v;
+  named_bar_sync(bar, kEpiThreads);
   return fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
 }
-__device__ __forceinline__ float epi_sum(float v, float* red) {
+__device__ __forceinline__ float epi_sum(float v, float* red, uint32_t bar) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  named_bar_sync(kEpiBar, kEpiThreads);
-  if (lane_id() == 0) red[warp_id() - 4] = v;
-  named_bar_sync(kEpiBar, kEpiThreads);
+  named_bar_sync(bar, kEpiThreads);
+  if (lane_id() == 0) red[warp_id() & 3] = v;
+  named_bar_sync(bar, kEpiThreads);
   return (red[0] + red[1]) + (red[2] + red[3]);
 }
-__device__ __forceinline__ int epi_prefix(bool pred, int* ired, int* total) {
-  const int w = warp_id() - 4, l = lane_id();
+__device__ __forceinline__ int epi_prefix(bool pred, int* ired, int* total, uint32_t bar) {
+  const int w = warp_id() & 3, l = lane_id();
   const unsigned bal = __ballot_sync(0xffffffffu, pred);
-  named_bar_sync(kEpiBar, kEpiThreads);
+  named_bar_sync(bar, kEpiThreads);
   if (l == 0) ired[w] = __popc(bal);
-  named_bar_sync(kEpiBar, kEpiThreads);
+  named_bar_sync(bar, kEpiThreads);
   int before = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) before += (i < w) ? ired[i] : 0;
@@ -104,8 +105,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto& s = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                      ~uintptr_t(1023));
   const Dims& D = prm.D;
-  float* m_s = reinterpret_cast<float*>(&s + 1);
-  float* S_s = m_s + D.M;
+
   const uint32_t warp = warp_id(), lane = lane_id();
 
   if (threadIdx.x == 0) {
@@ -119,17 +119,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&s.kb_full[i]), 1);
       mbar_init(smem_u32(&s.kb_empty[i]), 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(smem_u32(&s.d_full[i]), 1);
       mbar_init(smem_u32(&s.d_empty[i]), 4);  // one arrive per epilogue warp
     }
     for (int i = 0; i < kItemRing; ++i) {
       mbar_init(smem_u32(&s.it_full[i]), 1);
-      mbar_init(smem_u32(&s.it_empty[i]), 1 + 4);  // MMA thread + epilogue warps
+      mbar_init(smem_u32(&s.it_empty[i]), 1 + 4);  // MMA thread + the owning epilogue warpgroup
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<256>(smem_u32(&s.tmem_base));
+  if (warp == 2) tmem_alloc<512>(smem_u32(&s.tmem_base));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -146,7 +146,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (item >= prm.num_items) item = -1;
         s.items[slot] = item;
         mbar_arrive(smem_u32(&s.it_full[slot]));
-        if (item < 0) break;
+        if (item < 0) {  // the other epilogue warpgroup needs its own end marker
+          const int t2 = t + 1, slot2 = t2 % kItemRing;
+          if (t2 >= kItemRing) mbar_wait(smem_u32(&s.it_empty[slot2]), ((t2 / kItemRing) - 1) & 1);
+          s.items[slot2] = -1;
+          mbar_arrive(smem_u32(&s.it_full[slot2]));
+          break;
+        }
         int z, h, I;
         decode_item(D, item, z, h, I);
         const int zkv = z * D.Hkv + h / D.group;
@@ -175,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== MMA issuer (one thread)
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_bf16_f32(128, 128, false, false);
-      int gc = 0, dc = 0;
+      int gc = 0, dcw[2] = {0, 0};
       for (int t = 0;; ++t) {
         const int slot = t % kItemRing;
         mbar_wait(smem_u32(&s.it_full[slot]), (t / kItemRing) & 1);
@@ -184,11 +190,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (item < 0) break;
         int z, h, I;
         decode_item(D, item, z, h, I);
-        const int qb = t % kQBuf;
+        const int qb = t % kQBuf, wg = t & 1;
         mbar_wait(smem_u32(&s.q_full[qb]), (t / kQBuf) & 1);
         const int nchunks = I / kBlock + 1;
-        for (int c = 0; c < nchunks; ++c, ++gc, ++dc) {
-          const int st = gc % kStages, buf = dc & 1;
+        for (int c = 0; c < nchunks; ++c, ++gc, ++dcw[wg]) {
+          const int dc = dcw[wg];
+          const int st = gc % kStages, buf = wg * 2 + (dc & 1);
           if (dc >= 2) mbar_wait(smem_u32(&s.d_empty[buf]), ((dc >> 1) - 1) & 1);
           mbar_wait(smem_u32(&s.kb_full[st]), (gc / kStages) & 1);
           tc_fence_after();
@@ -213,13 +220,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue (128 threads)
-    const int et = threadIdx.x - 128;        // 0..127
-    const int jl = et;                       // TMEM lane == key block within a chunk
-    const uint32_t lane_addr = static_cast<uint32_t>((warp - 4) * 32) << 16;
+    // ===================== epilogue: two warpgroups, items alternate between them
+    const int wg = (warp - 4) >> 2;
+    const uint32_t ebar = kEpiBar + wg;
+    float* red = s.red[wg];
+    int* ired = s.ired[wg];
+    float* m_s = reinterpret_cast<float*>(&s + 1) + (size_t)wg * 2 * D.M;
+    float* S_s = m_s + D.M;
+    const int et = (threadIdx.x - 128) & 127;  // 0..127 within the warpgroup
+    const int jl = et;                         // TMEM lane == key block within a chunk
+    const uint32_t lane_addr = static_cast<uint32_t>(((warp - 4) & 3) * 32) << 16;
     const int N = D.M;
     int dc = 0;
-    for (int t = 0;; ++t) {
+    for (int t = wg;; t += 2) {
       const int slot = t % kItemRing;
       mbar_wait(smem_u32(&s.it_full[slot]), (t / kItemRing) & 1);
       const int item = s.items[slot];
@@ -233,11 +246,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       // ---- per chunk: TMEM row J -> (local max m, energy S)  (discovery.hpp:96-110)
       for (int c = 0; c < nchunks; ++c, ++dc) {
-        const int buf = dc & 1;
+        const int buf = wg * 2 + (dc & 1);
         mbar_wait(smem_u32(&s.d_full[buf]), (dc >> 1) & 1);
         tc_fence_after();
         const int J = c * kBlock + jl;
-        const bool warp_live = c * kBlock + (int)(warp - 4) * 32 <= I;  // warp-uniform
+        const bool warp_live = c * kBlock + (int)((warp - 4) & 3) * 32 <= I;  // warp-uniform
         float m = kNegSentinel, S = 0.f;
         if (warp_live) {
           uint32_t v[128];
@@ -277,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           S_s[J] = S;
         }
       }
-      named_bar_sync(kEpiBar, kEpiThreads);
+      named_bar_sync(ebar, kEpiThreads);
 
       // ---- outputs: energy / local_max rows, normalisation (discovery.hpp:131-143)
       const size_t map_row = (((size_t)z * D.Hq + h) * D.M + I) * (size_t)N;
@@ -290,14 +303,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (prm.out.normalize) {
         float rmax = kNegSentinel;
         for (int J = et; J <= I; J += kEpiThreads) rmax = fmaxf(rmax, m_s[J]);
-        rmax = epi_max(rmax, s.red);
+        rmax = epi_max(rmax, red, ebar);
         float total = 0.f;
         for (int J = et; J <= I; J += kEpiThreads) {
           const float r = __fmul_rn(S_s[J], ex2_approx(__fsub_rn(m_s[J], rmax)));
           S_s[J] = r;
           total += r;
         }
-        total = epi_sum(total, s.red);
+        total = epi_sum(total, red, ebar);
         const float inv = __fdiv_rn(1.0f, __fadd_rn(total, D.eps));
         float smax = 0.0f;  // selection.hpp:75
         for (int J = et; J <= I; J += kEpiThreads) {
@@ -311,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
         // ---- fused max-threshold + compaction (selection.hpp:63-92, 176-192)
         if (prm.out.idx || prm.out.mask) {
-          smax = epi_max(smax, s.red);
+          smax = epi_max(smax, red, ebar);
           const float thresh = __fmul_rn(D.alpha, smax);
           const size_t plan_row = ((size_t)z * D.M + I) * (size_t)N;  // [z, I, :, :]
           int base = 0;
@@ -320,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             bool act = false;
             if (J <= I) act = (S_s[J] >= thresh) || J < D.sink_blocks || (I - J) < D.window_blocks;
             int tot;
-            const int slot_j = base + epi_prefix(act, s.ired, &tot);
+            const int slot_j = base + epi_prefix(act, ired, &tot, ebar);
             if (prm.out.mask && J < N) prm.out.mask[(plan_row + J) * D.Hq + h] = act ? 1 : 0;
             if (prm.out.idx && act) prm.out.idx[(plan_row + slot_j) * D.Hq + h] = J;
             base += tot;
@@ -335,17 +348,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             prm.out.counts[((size_t)z * D.M + I) * D.Hq + h] = base;
         }
       }
-      named_bar_sync(kEpiBar, kEpiThreads);  // m_s / S_s free for the next item
+      named_bar_sync(ebar, kEpiThreads);  // m_s / S_s free for the next item
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) tmem_dealloc<256>(tmem);
+  if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
 template <int NQ>
 size_t disc_smem_bytes(int M) {
-  return sizeof(DiscSmem<NQ>) + 1024 + 2 * sizeof(float) * (size_t)M;
+  return sizeof(DiscSmem<NQ>) + 1024 + 4 * sizeof(float) * (size_t)M;
 }
 
 template <int NQ>

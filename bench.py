@@ -175,6 +175,10 @@ def run_reference_arm(args, rank, world):
 
 
 # ------------------------------------------------------------------------------ GPU arm
+def _coll_device(dist, dev):
+    return torch.device("cpu") if dist.get_backend() == "gloo" else dev
+
+
 def run_gpu_arm(args, rank, world, dist):
     import paper_2603_06199_b200 as fp
 
@@ -220,8 +224,8 @@ def run_gpu_arm(args, rank, world, dist):
             dist.barrier()
     ms = statistics.mean(t_step)
     ms_disc, ms_attn = statistics.mean(t_disc), statistics.mean(t_attn)
-    if dist:
-        tt = torch.tensor([ms, ms_disc, ms_attn], device=dev)
+    if dist:  # max over ranks
+        tt = torch.tensor([ms, ms_disc, ms_attn], device=_coll_device(dist, dev))
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms, ms_disc, ms_attn = (float(x) for x in tt.tolist())
 
@@ -262,7 +266,7 @@ def run_gpu_arm(args, rank, world, dist):
             times.append((time.perf_counter() - t0) * 1e3)
         e2e_ms = statistics.mean(times)
         if dist:
-            tt = torch.tensor([e2e_ms], device=dev)
+            tt = torch.tensor([e2e_ms], device=_coll_device(dist, dev))
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_ms = float(tt.item())
 
@@ -348,8 +352,13 @@ def main():
     dist = None
     if world > 1 and args.impl == "fpb200":
         import torch.distributed as tdist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        tdist.init_process_group("nccl")
+        if os.environ.get("FPB_BENCH_SHARED_GPU"):
+            # test mode for 1-GPU boxes: every rank on cuda:0, timing collectives over gloo
+            os.environ["LOCAL_RANK"] = "0"
+            tdist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+            tdist.init_process_group("nccl")
         dist = tdist
     if args.impl == "reference":
         run_reference_arm(args, rank, world)

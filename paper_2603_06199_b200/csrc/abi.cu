@@ -125,10 +125,12 @@ DiscWs disc_ws(const Dims& D, void* ws) {
   return {reinterpret_cast<int*>(w), reinterpret_cast<__nv_bfloat16*>(w + kSchedBytes),
           reinterpret_cast<__nv_bfloat16*>(w + kSchedBytes + align_up(kbar_split_bytes(D)))};
 }
-size_t ws_attention(const Dims& D, fpb_dtype t) {  // [sched] + fp32: Q hi/lo, K hi/lo, V bf16
-  return kSchedBytes + (t == FPB_F32 ? align_up(2 * q_elems(D) * 2) +
-                                           align_up(2 * kv_elems(D) * 2) + align_up(kv_elems(D) * 2)
-                                     : 0);
+// attention: [sched][plan-row scratch] + fp32: Q hi/lo, K hi/lo, V bf16
+size_t ws_attention(const Dims& D, fpb_dtype t) {
+  return kSchedBytes + align_up(attention_list_bytes(D)) +
+         (t == FPB_F32 ? align_up(2 * q_elems(D) * 2) + align_up(2 * kv_elems(D) * 2) +
+                             align_up(kv_elems(D) * 2)
+                       : 0);
 }
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -332,7 +334,7 @@ static int attention_common(const fpb_problem* p, fpb_dtype dtype, const void* Q
                       *k = static_cast<const __nv_bfloat16*>(K),
                       *v = static_cast<const __nv_bfloat16*>(V);
   if (dtype == FPB_F32) {
-    uint8_t* w = static_cast<uint8_t*>(workspace) + kSchedBytes;
+    uint8_t* w = static_cast<uint8_t*>(workspace) + kSchedBytes + align_up(attention_list_bytes(D));
     __nv_bfloat16* q2 = reinterpret_cast<__nv_bfloat16*>(w);
     __nv_bfloat16* k2 = reinterpret_cast<__nv_bfloat16*>(w + align_up(2 * q_elems(D) * 2));
     __nv_bfloat16* v2 = reinterpret_cast<__nv_bfloat16*>(w + align_up(2 * q_elems(D) * 2) +
@@ -348,7 +350,10 @@ static int attention_common(const fpb_problem* p, fpb_dtype dtype, const void* Q
   }
 FPB_CUDA(launch_attention(D, dtype == FPB_F32 ? 2 : 1, q, k, v, idx, counts,
                             out_dtype == FPB_BF16, out, lse, visits, plan_error,
-                            static_cast<int*>(workspace), S(stream)));
+                            static_cast<int*>(workspace),
+                            reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(workspace) +
+                                                        kSchedBytes),
+                            S(stream)));
   return FPB_OK;
 }
 

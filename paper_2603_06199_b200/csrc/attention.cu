@@ -360,10 +360,10 @@ cudaError_t launch_attention(const Dims& D, int splits, const __nv_bfloat16* Q,
                              const __nv_bfloat16* K, const __nv_bfloat16* V, const int32_t* idx,
                              const int32_t* counts, bool out_bf16, void* out, float* lse,
                              unsigned long long* visits, int32_t* plan_error, int* sched,
-                             cudaStream_t s) {
+                             uint16_t* lists, cudaStream_t s) {
   if (splits == 1)
     return launch_attention_fa(D, Q, K, V, idx, counts, out_bf16, out, lse, visits, plan_error,
-                               sched, s);
+                               sched, lists, s);
   CUtensorMap tm_q, tm_k, tm_v;
   if (!make_tmap_rows128(&tm_q, Q, D.L, (uint64_t)splits * D.Z * D.Hq) ||
       !make_tmap_rows128(&tm_k, K, D.L, (uint64_t)splits * D.Z * D.Hkv) ||
@@ -372,5 +372,7 @@ cudaError_t launch_attention(const Dims& D, int splits, const __nv_bfloat16* Q,
   AttnParams prm{D, idx, counts, out, lse, visits, plan_error, out_bf16 ? 1 : 0};
   return launch_ns<2>(D, tm_q, tm_k, tm_v, prm, s);
 }
+
+size_t attention_list_bytes(const Dims& D) { return (size_t)256 * 4 * D.M * sizeof(uint16_t); }
 
 }  // namespace fpb

@@ -11,8 +11,10 @@
 //   TMEM (512 cols): S0 | S1 | O0 | O1; P (bf16) is written back over S and read by the PV MMA
 //   straight from TMEM (ts form).  Issue order per slot unit: PV(j-1) then QK(j) — in-order
 //   tcgen05 execution makes the S/P aliasing safe.
-//   SMEM: Q0, Q1 (32 KiB each) + a 4-tile K/V ring shared by both slots, filled by TMA in exactly
-//   the MMA consumption order (both warps run the same deterministic unit schedule).
+//   SMEM: Q0, Q1 (32 KiB each) + a 5-tile K/V ring shared by both slots, filled by TMA in exactly
+//   the MMA consumption order (both warps run the same deterministic unit schedule).  At the end
+//   of an item the slot's Q tile is the staging buffer of the O tile, written by one TMA store.
+//   Compacted plan rows live in a global scratch (L2-resident), not in SMEM.
 //
 // Warps: w0 TMA producer; w1 MMA issuer; w2 TMEM allocator; w3 scheduler (dynamic work counter,
 // plan-row fetch + range check + compaction, two items ahead per slot); w4..w7 softmax/epilogue
@@ -28,7 +30,7 @@ namespace {
 
 constexpr int kThreads = 384;
 constexpr int kTile = kBlock * kHeadDim * 2;  // 32 KiB bf16 tile
-constexpr int kRing = 4;                      // shared K/V tile ring
+constexpr int kRing = 5;                      // shared K/V tile ring
 constexpr float kRescaleThreshold = 8.0f;     // lazy O rescale (log2 units)
 #ifndef FPB_POLY_MASK
 #define FPB_POLY_MASK 0  // pairs p with (p & 3) in this bit mask use exp2_poly2 (FMA pipe)
@@ -43,9 +45,34 @@ struct FaParams {
   unsigned long long* visits;
   int32_t* plan_error;
   int* sched;
+  uint16_t* lists;  // global scratch: [grid][2 slots][2 bufs][M] compacted plan rows
   int num_items;
   int out_bf16;
 };
+
+#ifdef FPB_TRACE
+// cycle accounting (tools/trace_attention.py): per-warp register accumulators, flushed once
+__device__ unsigned long long g_trace[16];
+#define TR_DECL unsigned long long tr_acc[16] = {}
+#define TR_T0() long long _tr = clock64()
+#define TR_ADD(i)                                  \
+  do {                                             \
+    const long long _n = clock64();                \
+    tr_acc[i] += (unsigned long long)(_n - _tr);   \
+    _tr = _n;                                      \
+  } while (0)
+#define TR_FLUSH()                                                          \
+  do {                                                                      \
+    if (lane_id() == 0)                                                     \
+      for (int _i = 0; _i < 16; ++_i)                                       \
+        if (tr_acc[_i]) atomicAdd(&g_trace[_i], tr_acc[_i]);                \
+  } while (0)
+#else
+#define TR_DECL
+#define TR_T0()
+#define TR_ADD(i)
+#define TR_FLUSH()
+#endif
 
 struct SlotMeta {
   int item;  // -1: no more work
@@ -61,7 +88,6 @@ struct FaSmem {
   uint64_t meta_full[2][2], meta_empty[2][2];
   SlotMeta meta[2][2];
   uint32_t tmem_base;
-  // followed by uint16_t list[2 slots][2 bufs][M] (sparse only)
 };
 
 __device__ __forceinline__ void decode(const Dims& D, int item, int& z, int& h, int& qi) {
@@ -84,21 +110,24 @@ struct SlotState {
 
 __global__ void __launch_bounds__(kThreads, 1)
     fa_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-              const __grid_constant__ CUtensorMap tm_v, const FaParams prm) {
+              const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+              const FaParams prm) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   auto& s = *reinterpret_cast<FaSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                        ~uintptr_t(1023));
   const Dims& D = prm.D;
   const int N = D.M;
-  uint16_t* lists = reinterpret_cast<uint16_t*>(&s + 1);
+  uint16_t* lists = prm.lists + (size_t)blockIdx.x * 4 * D.M;
   auto list_of = [&](int slot, int p) { return lists + (size_t)(slot * 2 + p) * D.M; };
   const bool dense = prm.idx == nullptr;
   const uint32_t warp = warp_id(), lane = lane_id();
+  TR_DECL;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_o);
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&s.q_full[i]), 1);
       mbar_init(smem_u32(&s.q_empty[i]), 1);
@@ -186,7 +215,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int kvc = 0;  // tiles pushed through the ring
     auto push = [&](const CUtensorMap* map, int row, int plane) {
       const int r = kvc % kRing;
+      TR_T0();
       if (kvc >= kRing) mbar_wait(smem_u32(&s.kv_empty[r]), ((kvc / kRing) - 1) & 1);
+      TR_ADD(12);  // producer: waiting for a free ring slot
       if (lane == 0) {
         const uint32_t fb = smem_u32(&s.kv_full[r]);
         mbar_arrive_expect_tx(fb, kTile);
@@ -203,7 +234,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!S.active) continue;
         const int p = S.t & 1;
         if (S.j == 0) {
-          mbar_wait(smem_u32(&s.meta_full[sl][p]), (S.t >> 1) & 1);
+          {
+            TR_T0();
+            mbar_wait(smem_u32(&s.meta_full[sl][p]), (S.t >> 1) & 1);
+            TR_ADD(14);  // producer: waiting for the scheduler
+          }
           S.item = s.meta[sl][p].item;
           S.nblk = s.meta[sl][p].nblk;
           if (S.item < 0) {
@@ -216,7 +251,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           int z, h, qi;
           decode(D, S.item, z, h, qi);
-          if (S.qc >= 1) mbar_wait(smem_u32(&s.q_empty[sl]), (S.qc - 1) & 1);
+          {
+            TR_T0();
+            if (S.qc >= 1) mbar_wait(smem_u32(&s.q_empty[sl]), (S.qc - 1) & 1);
+            TR_ADD(13);  // producer: waiting for the slot's Q tile (previous epilogue)
+          }
           if (lane == 0) {
             const uint32_t qb = smem_u32(&s.q_full[sl]);
             mbar_arrive_expect_tx(qb, kTile);
@@ -265,7 +304,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++S.t;
             continue;
           }
-          mbar_wait(smem_u32(&s.q_full[sl]), S.qc & 1);
+          {
+            TR_T0();
+            mbar_wait(smem_u32(&s.q_full[sl]), S.qc & 1);
+            TR_ADD(15);  // MMA: waiting for Q
+          }
           ++S.qc;
         }
         if (S.j >= 1) {
@@ -273,12 +316,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int m = S.j - 1;
           if (m == 0 && S.qc >= 2) mbar_wait(smem_u32(&s.o_free[sl]), (S.qc - 2) & 1);
           const int r = kvc % kRing;
+          TR_T0();
           mbar_wait(smem_u32(&s.kv_full[r]), (kvc / kRing) & 1);
+          TR_ADD(8);  // MMA: waiting for V
           const uint32_t vb = smem_u32(s.ring[r]);
           // keys 0..63 as soon as the first half of P is in TMEM, keys 64..127 after the rest
           for (int half = 0; half < 2; ++half) {
             mbar_wait(smem_u32(half ? &s.p_full[sl] : &s.p_half[sl]), (S.bc - 1) & 1);
             tc_fence_after();
+            TR_ADD(9 + half);  // MMA: waiting for P half
             if (leader) {
 #pragma unroll
               for (int k4 = 0; k4 < 4; ++k4) {
@@ -299,8 +345,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (S.j < S.nblk) {
           // QK(j): S_sl = Q_sl K(j)^T
           const int r = kvc % kRing;
+          TR_T0();
           mbar_wait(smem_u32(&s.kv_full[r]), (kvc / kRing) & 1);
           tc_fence_after();
+          TR_ADD(11);  // MMA: waiting for K
           if (leader) {
             const uint32_t qb = smem_u32(s.q[sl]), kb = smem_u32(s.ring[r]);
 #pragma unroll
@@ -311,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             mma_commit(smem_u32(&s.kv_empty[r]));
             mma_commit(smem_u32(&s.s_full[sl]));
-            if (S.j == S.nblk - 1) mma_commit(smem_u32(&s.q_empty[sl]));
+
           }
           __syncwarp();
           ++kvc;
@@ -349,13 +397,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cols = block_len(D, kv);
         const int lim = (kv == qi) ? min(cols, r + 1) : cols;  // attention.hpp:85-91
         const bool full = __all_sync(0xffffffffu, lim == kBlock);
+        TR_T0();
         mbar_wait(smem_u32(&s.s_full[sl]), bc & 1);
         tc_fence_after();
+        TR_ADD(0);  // softmax: waiting for S
         uint32_t v[128];
-        tmem_ld32(s_addr + 0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-        tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
-        tmem_ld32(s_addr + 64, *reinterpret_cast<uint32_t(*)[32]>(&v[64]));
-        tmem_ld32(s_addr + 96, *reinterpret_cast<uint32_t(*)[32]>(&v[96]));
+        tmem_ld64(s_addr + 0, &v[0]);
+        tmem_ld64(s_addr + 64, &v[64]);
         tmem_ld_wait();
         if (!full) {
 #pragma unroll
@@ -372,6 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
         const float m_new = fmaxf(m_used, mx * D.to_bits);
+        TR_ADD(1);  // softmax: TMEM load + mask + row max
         if (n == 0) {
           m_used = m_new;
         } else if (__any_sync(0xffffffffu, m_new > m_used + kRescaleThreshold)) {
@@ -391,6 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           l *= f;
           m_used = m_new;
         }
+        TR_ADD(2);  // softmax: lazy O rescale (rare)
         const float neg_m = -m_used, sc = D.to_bits;
         float bs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -427,15 +477,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(half ? &s.p_full[sl] : &s.p_half[sl]));
+          TR_ADD(3 + half);  // softmax: exp + pack + TMEM store, per half
         }
         l += ((bs[0] + bs[1]) + (bs[2] + bs[3])) + ((bs[4] + bs[5]) + (bs[6] + bs[7]));
       }
+      TR_T0();
       // ---- epilogue (attention.hpp:119-126)
       const size_t orow = ((size_t)z * D.Hq + h) * (size_t)D.L + (size_t)qi * kBlock + r;
       if (nblk > 0) {
-        mbar_wait(smem_u32(&s.o_done[sl]), (bc - 1) & 1);
+        mbar_wait(smem_u32(&s.o_done[sl]), (bc - 1) & 1);  // last PV done => last QK done too
         tc_fence_after();
         const float inv = 1.0f / l;
+        const uint32_t stage = smem_u32(s.q[sl]);  // this slot's Q tile is free: O staging
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
           uint32_t o[32];
@@ -446,30 +499,48 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&s.o_free[sl]));
           }
-          if (r < rows) {
-            if (prm.out_bf16) {
-              uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(prm.out) +
+          if (prm.out_bf16) {
+            // row r, columns 32cc..32cc+31 -> SW128 tile layout of the TMA box (64 cols x 128 rows)
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const int col = cc * 32 + q4 * 8;
+              const uint32_t off = (col >> 6) * (kTile / 2) + r * 128 +
+                                   ((((col & 63) >> 3) ^ (r & 7)) << 4);
+              const uint4 val = make_uint4(
+                  pack_bf16x2(__uint_as_float(o[8 * q4 + 0]) * inv, __uint_as_float(o[8 * q4 + 1]) * inv),
+                  pack_bf16x2(__uint_as_float(o[8 * q4 + 2]) * inv, __uint_as_float(o[8 * q4 + 3]) * inv),
+                  pack_bf16x2(__uint_as_float(o[8 * q4 + 4]) * inv, __uint_as_float(o[8 * q4 + 5]) * inv),
+                  pack_bf16x2(__uint_as_float(o[8 * q4 + 6]) * inv, __uint_as_float(o[8 * q4 + 7]) * inv));
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stage + off),
+                           "r"(val.x), "r"(val.y), "r"(val.z), "r"(val.w)
+                           : "memory");
+            }
+          } else if (r < rows) {
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(prm.out) +
                                                     orow * kHeadDim + cc * 32);
 #pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4)
-                dst[q4] = make_uint4(
-                    pack_bf16x2(__uint_as_float(o[8 * q4 + 0]) * inv, __uint_as_float(o[8 * q4 + 1]) * inv),
-                    pack_bf16x2(__uint_as_float(o[8 * q4 + 2]) * inv, __uint_as_float(o[8 * q4 + 3]) * inv),
-                    pack_bf16x2(__uint_as_float(o[8 * q4 + 4]) * inv, __uint_as_float(o[8 * q4 + 5]) * inv),
-                    pack_bf16x2(__uint_as_float(o[8 * q4 + 6]) * inv, __uint_as_float(o[8 * q4 + 7]) * inv));
-            } else {
-              float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(prm.out) +
-                                                      orow * kHeadDim + cc * 32);
-#pragma unroll
-              for (int q4 = 0; q4 < 8; ++q4)
-                dst[q4] = make_float4(__uint_as_float(o[4 * q4]) * inv,
-                                      __uint_as_float(o[4 * q4 + 1]) * inv,
-                                      __uint_as_float(o[4 * q4 + 2]) * inv,
-                                      __uint_as_float(o[4 * q4 + 3]) * inv);
-            }
+            for (int q4 = 0; q4 < 8; ++q4)
+              dst[q4] = make_float4(__uint_as_float(o[4 * q4]) * inv,
+                                    __uint_as_float(o[4 * q4 + 1]) * inv,
+                                    __uint_as_float(o[4 * q4 + 2]) * inv,
+                                    __uint_as_float(o[4 * q4 + 3]) * inv);
           }
         }
         if (r < rows) prm.lse[orow] = m_used + log2f(l);
+        if (prm.out_bf16) {
+          fence_proxy_async_smem();
+          named_bar_sync(1 + sl, 128);
+          if (r == 0) {  // rows beyond L are clipped by the tensor map
+            tma_store_3d(&tm_o, stage, 0, qi * kBlock, z * D.Hq + h);
+            tma_store_3d(&tm_o, stage + kTile / 2, 64, qi * kBlock, z * D.Hq + h);
+            bulk_commit();
+            bulk_wait_read0();
+            mbar_arrive(smem_u32(&s.q_empty[sl]));
+          }
+        } else {
+          named_bar_sync(1 + sl, 128);  // every thread is past its tcgen05.ld of O
+          if (r == 0) mbar_arrive(smem_u32(&s.q_empty[sl]));
+        }
         ++qc;
       } else if (r < rows) {  // C = 0: out = 0 * (1/0) = NaN, lse = -inf (attention.hpp:121-125)
         const float nan = __int_as_float(0x7fc00000);
@@ -483,11 +554,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         prm.lse[orow] = -INFINITY;
       }
+      TR_ADD(5);  // softmax warps: item epilogue
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&s.meta_empty[sl][p]));
     }
     (void)qc;
   }
+  TR_FLUSH();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<512>(tmem);
@@ -498,25 +571,38 @@ __global__ void __launch_bounds__(kThreads, 1)
 cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __nv_bfloat16* K,
                                 const __nv_bfloat16* V, const int32_t* idx, const int32_t* counts,
                                 bool out_bf16, void* out, float* lse, unsigned long long* visits,
-                                int32_t* plan_error, int* sched, cudaStream_t s) {
-  CUtensorMap tm_q, tm_k, tm_v;
+                                int32_t* plan_error, int* sched, uint16_t* lists, cudaStream_t s) {
+  CUtensorMap tm_q, tm_k, tm_v, tm_o;
   if (!make_tmap_rows128(&tm_q, Q, D.L, (uint64_t)D.Z * D.Hq) ||
       !make_tmap_rows128(&tm_k, K, D.L, (uint64_t)D.Z * D.Hkv) ||
-      !make_tmap_rows128(&tm_v, V, D.L, (uint64_t)D.Z * D.Hkv))
+      !make_tmap_rows128(&tm_v, V, D.L, (uint64_t)D.Z * D.Hkv) ||
+      !make_tmap_rows128(&tm_o, out_bf16 ? out : Q, D.L, (uint64_t)D.Z * D.Hq))
     return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(sched, 0, sizeof(int), s);
-  if (e != cudaSuccess) return e;
-  FaParams prm{D, idx, counts, out, lse, visits, plan_error, sched, D.Z * D.Hq * D.M,
-               out_bf16 ? 1 : 0};
-  const size_t smem = sizeof(FaSmem) + 1024 + (idx ? 4 * sizeof(uint16_t) * (size_t)D.M : 0);
-  e = cudaFuncSetAttribute(fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = prm.num_items < sms ? prm.num_items : sms;
-  fa_kernel<<<grid, kThreads, smem, s>>>(tm_q, tm_k, tm_v, prm);
+  const int num_items = D.Z * D.Hq * D.M;
+  const int grid = num_items < sms ? num_items : sms;
+  FaParams prm{D, idx, counts, out, lse, visits, plan_error, sched, lists, num_items,
+               out_bf16 ? 1 : 0};
+  const size_t smem = sizeof(FaSmem) + 1024;
+  e = cudaFuncSetAttribute(fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fa_kernel<<<grid, kThreads, smem, s>>>(tm_q, tm_k, tm_v, tm_o, prm);
   return cudaGetLastError();
 }
 
 }  // namespace fpb
+
+#ifdef FPB_TRACE
+extern "C" int fpb_trace_read(unsigned long long* host16, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(host16, fpb::g_trace, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(fpb::g_trace, z, sizeof(z));
+  }
+  return (int)e;
+}
+#endif

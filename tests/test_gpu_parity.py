@@ -286,3 +286,37 @@ def test_golden_reference_vectors(fp, port, path):
     if "out_dense" in g.files:
         res = fp.dense_attention(_cuda(q), _cuda(k), _cuda(v), tau, out_dtype=torch.float32)
         _attn_check(_np(res.out), _np(res.lse), g["out_dense"], g["lse_dense"])
+
+
+# --------------------------------------------------------------------------- full-size properties
+def test_qwen3_32k_plan_invariants_and_full_plan_identity(fp):
+    """BASELINE config 2 at full size: plan invariants (selection.hpp:176-192 + :53-56) and the
+    size-independent identity sparse(full causal plan) == dense (acceptance.cpp crit. 1)."""
+    from paper_2603_06199_b200 import workload
+    L = 32768
+    q, k, v = (x.cuda() for x in workload.qwen3_30b_a3b(L, seed=3))
+    cfg = fp.PipelineConfig()
+    plan, _, mask = fp.discover_select(q, k, cfg, want_mask=True)
+    M = L // 128
+    idx, counts = plan.indices.long(), plan.counts.long()
+    slot = torch.arange(M, device="cuda").view(1, 1, M, 1)
+    within = slot < counts.view(1, M, 1, 32)
+    # strictly increasing active prefix, fill value N after it, counts in [min retained, i+1]
+    assert torch.all((idx[..., :-1, :] < idx[..., 1:, :]) | ~within[..., 1:, :])
+    assert torch.all(torch.where(within, True, idx == M))
+    i = torch.arange(M, device="cuda").view(1, M, 1)
+    assert torch.all(counts <= i + 1) and torch.all(counts >= torch.clamp(i + 1, max=6))
+    # mask <-> plan round trip, and retention of sink / window / diagonal blocks
+    assert torch.equal(mask.active.sum(dim=2).long(), counts)
+    diag = mask.active[0, torch.arange(M), torch.arange(M), :]
+    assert torch.all(diag == 1)
+    assert torch.all(mask.active[0, 2:, :2, :] == 1)
+    grid = fp.make_block_grid(L, 128)
+    tau = cfg.resolved_scale(128)
+    full = fp.full_causal_plan(1, 32, grid)
+    a = fp.block_sparse_attention(q, k, v, full, grid, tau, out_dtype=torch.float32)
+    b = fp.dense_attention(q, k, v, tau, out_dtype=torch.float32)
+    assert torch.equal(a.out, b.out) and torch.equal(a.lse, b.lse)
+    st = fp.AttentionStats()
+    fp.block_sparse_attention(q, k, v, plan, grid, tau, st)
+    assert st.block_visits == int(counts.sum())

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -654,8 +655,10 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
   if (rc || (rc = check_dtype(dtype)) || (rc = check_dtype(out_dtype))) return rc;
   if (!Q || !K || !V || !out || !lse) return fail(FPB_EUSAGE, "null pointer");
   const int group = D.Hq / D.Hkv;
-  int cq = group;  // Q heads per chunk: at least 8 chunks when the problem allows it
-  while (cq % 2 == 0 && (int64_t)D.Z * D.Hq / cq < 8) cq /= 2;
+  int min_chunks = 16;  // Q heads per chunk: at least 16 chunks when the problem allows it
+  if (const char* e = getenv("FPB_E2E_CHUNKS")) min_chunks = atoi(e);
+  int cq = group;
+  while (cq % 2 == 0 && (int64_t)D.Z * D.Hq / cq < min_chunks) cq /= 2;
   const int chunks_per_z = D.Hq / cq, nch = D.Z * chunks_per_z;
   const size_t es = dsz(dtype), eo = dsz(out_dtype), Ld = (size_t)D.L * kHeadDim;
   const size_t qb = q_elems(D) * es, kb = kv_elems(D) * es, ob = q_elems(D) * eo,

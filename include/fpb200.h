@@ -116,6 +116,24 @@ int fpb_dense_attention(const fpb_problem* p, fpb_dtype dtype, const void* Q, co
 /* full_causal_plan (attention.hpp:178-192). */
 int fpb_full_causal_plan(const fpb_problem* p, int32_t* idx, int32_t* counts, void* stream);
 
+/* ---- Comparison baselines of the reference (not on the FlashPrefill path) ---------------- */
+/* topk_select (selection.hpp:96-123): min(k, i+1) highest scores per causal row, ties toward the
+ * lower block index, plus sink/window retention.  Rows up to 4096 blocks. */
+int fpb_topk_select(const fpb_problem* p, const float* score, int32_t k, uint8_t* mask,
+                    void* stream);
+/* topp_select (selection.hpp:127-159): shortest descending prefix reaching mass p (0 < p <= 1). */
+int fpb_topp_select(const fpb_problem* p, const float* score, float top_p, uint8_t* mask,
+                    void* stream);
+/* discover_pool_both (discovery.hpp:164-195) and discover_exact (discovery.hpp:201-279).
+ * Scratch: fpb_baseline_workspace_bytes. */
+int fpb_baseline_workspace_bytes(const fpb_problem* p, size_t* bytes);
+int fpb_discover_pool_both(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                           float* energy, float* local_max, float* score, void* workspace,
+                           size_t workspace_bytes, void* stream);
+int fpb_discover_exact(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                       float* energy, float* local_max, float* score, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
 /* ---- Host-buffer entry points (copy in, run, copy out, synchronise) ----------------------- */
 int fpb_host_pool_keys(const fpb_problem* p, fpb_dtype dtype, const void* K, float* pooled);
 int fpb_host_approx_block_scores(const fpb_problem* p, fpb_dtype dtype, const void* Q,
@@ -126,6 +144,11 @@ int fpb_host_discover(const fpb_problem* p, fpb_dtype dtype, const void* Q, cons
                       float* energy, float* local_max, float* score);
 int fpb_host_max_threshold_mask(const fpb_problem* p, const float* score, uint8_t* mask,
                                 unsigned long long* comparisons);
+int fpb_host_topk_select(const fpb_problem* p, const float* score, int32_t k, uint8_t* mask);
+int fpb_host_topp_select(const fpb_problem* p, const float* score, float top_p, uint8_t* mask);
+/* method: 0 approx (== fpb_host_discover), 1 pool-both, 2 exact */
+int fpb_host_discover_method(const fpb_problem* p, fpb_dtype dtype, int method, const void* Q,
+                             const void* K, float* energy, float* local_max, float* score);
 int fpb_host_compress_indices(const fpb_problem* p, const uint8_t* mask, int32_t* idx,
                               int32_t* counts);
 int fpb_host_block_sparse_attention(const fpb_problem* p, fpb_dtype dtype, const void* Q,

@@ -8,8 +8,10 @@
 // to HBM, the kernels run, outputs come back.  Link with -lfpb200 (paper_2603_06199_b200/).
 //
 // Differences, all supersets: K/V may have fewer heads than Q (GQA; the reference requires equal
-// shapes, core.hpp:81-85); the kernels require d == 128 and block_size == 128 (ValidationError
-// otherwise).  fp32 inputs run the split-precision path (bf16 hi + lo) end to end.
+// shapes, core.hpp:81-85).  d == 128 with block_size == 128 runs the tcgen05 kernels (fp32 inputs
+// through the split-precision path); every other shape runs the SIMT kernels of generic.cu.
+// The comparison baselines (topk_select, topp_select, discover_pool_both, discover_exact) are here
+// too, so the whole bsattn surface is covered.
 #pragma once
 
 #include <cmath>
@@ -285,6 +287,36 @@ inline BlockScoreMap discover(const SequenceBatch& q, const SequenceBatch& k, co
   return m;
 }
 
+// comparison methods (discovery.hpp:164-279), method 1 = pool-both, 2 = exact
+namespace detail {
+inline BlockScoreMap discover_method(int method, const SequenceBatch& q, const SequenceBatch& k,
+                                     const BlockGrid& grid, float tau, float epsilon) {
+  require_qk(q, k);
+  auto p = problem(q.batch(), q.heads(), k.heads(), q.seq_len(), q.head_dim(), grid.block_size);
+  p.scale = tau;
+  p.epsilon = epsilon;
+  const std::uint64_t M = grid.num_query_blocks;
+  BlockScoreMap m{Tensor<float>({q.batch(), q.heads(), M, M}),
+                  Tensor<float>({q.batch(), q.heads(), M, M}),
+                  Tensor<float>({q.batch(), q.heads(), M, M})};
+  check(fpb_host_discover_method(&p, FPB_F32, method, q.data.data(), k.data.data(),
+                                 m.energy.data(), m.local_max.data(), m.score.data()),
+        method == 1 ? "discover_pool_both" : "discover_exact");
+  return m;
+}
+}  // namespace detail
+
+inline BlockScoreMap discover_pool_both(const SequenceBatch& q, const SequenceBatch& k,
+                                        const BlockGrid& grid, float tau,
+                                        float epsilon = kDefaultEpsilon) {
+  return detail::discover_method(1, q, k, grid, tau, epsilon);
+}
+inline BlockScoreMap discover_exact(const SequenceBatch& q, const SequenceBatch& k,
+                                    const BlockGrid& grid, float tau,
+                                    float epsilon = kDefaultEpsilon) {
+  return detail::discover_method(2, q, k, grid, tau, epsilon);
+}
+
 // ----------------------------------------------------------------------------- selection.hpp
 inline ActiveMask max_threshold_mask(const Tensor<float>& score, const PipelineConfig& config,
                                      SelectionStats* stats = nullptr) {
@@ -307,6 +339,42 @@ inline ActiveMask max_threshold_mask(const Tensor<float>& score, const PipelineC
 inline ActiveMask max_threshold_mask(const BlockScoreMap& scores, const PipelineConfig& config,
                                      SelectionStats* stats = nullptr) {
   return max_threshold_mask(scores.score, config, stats);
+}
+
+namespace detail {
+inline ActiveMask sort_select(const Tensor<float>& score, int mode, std::uint32_t k, float top_p,
+                              const PipelineConfig& config) {
+  config.validate();
+  if (score.ndim() != 4) throw ValidationError("score map must be Z x H x M x N");
+  const std::uint64_t Z = score.dim(0), H = score.dim(1), M = score.dim(2), N = score.dim(3);
+  auto p = problem(Z, H, H, (M - 1) * config.block_size + 1, 128, config.block_size);
+  p.sink_tokens = static_cast<int32_t>(config.sink_tokens);
+  p.window_tokens = static_cast<int32_t>(config.window_tokens);
+  ActiveMask mask{Tensor<std::uint8_t>({Z, M, N, H})};
+  const int rc = mode == 0 ? fpb_host_topk_select(&p, score.data(), static_cast<int32_t>(k),
+                                                  mask.active.data())
+                           : fpb_host_topp_select(&p, score.data(), top_p, mask.active.data());
+  if (rc == FPB_EVALIDATION) throw ConfigError(fpb_last_error());
+  check(rc, mode == 0 ? "topk_select" : "topp_select");
+  return mask;
+}
+}  // namespace detail
+
+// selection.hpp:96-123 / 127-159 (comparison baselines)
+inline ActiveMask topk_select(const Tensor<float>& score, std::uint32_t k,
+                              const PipelineConfig& config) {
+  if (k < 1) throw ConfigError("top-k requires k >= 1");
+  return detail::sort_select(score, 0, k, 0.0f, config);
+}
+inline ActiveMask topp_select(const Tensor<float>& score, float p, const PipelineConfig& config) {
+  if (!(p > 0.0f) || p > 1.0f) throw ConfigError("top-p requires p in (0, 1]");
+  return detail::sort_select(score, 1, 1, p, config);
+}
+inline ActiveMask topk_select(const BlockScoreMap& s, std::uint32_t k, const PipelineConfig& c) {
+  return topk_select(s.score, k, c);
+}
+inline ActiveMask topp_select(const BlockScoreMap& s, float p, const PipelineConfig& c) {
+  return topp_select(s.score, p, c);
 }
 
 inline SparseBlockPlan compress_indices(const ActiveMask& mask) {

@@ -82,6 +82,18 @@ class Oracle:
         gp("pipeline_threads").argtypes = [_p, _p, _p, _u64, _u64, _u64, _u64, _u64, _u32, _f32,
                                            _u32, _u32, _f32, _f32, _p, _i32, _i32, _p, _p, _p]
         gp("pipeline_threads").restype = C.c_double
+        gp("topk_select").argtypes = [_p, _u64, _u64, _u32, _u32, _u32, _u32, _u32, _p]
+        gp("topp_select").argtypes = [_p, _u64, _u64, _u32, _f32, _u32, _u32, _u32, _p]
+        if pre == "or_":
+            gp("discover_pool_both").argtypes = [_p, _p, _u64, _u64, _u64, _u64, _u64, _u32, _f32,
+                                                 _f32, _p, _p, _p]
+            gp("discover_exact").argtypes = [_p, _p, _u64, _u64, _u64, _u64, _u64, _u32, _f32,
+                                             _f32, _p, _p, _p]
+        else:
+            gp("discover_pool_both").argtypes = [_p, _p, _u64, _u64, _u64, _u64, _u32, _f32, _f32,
+                                                 _p, _p, _p]
+            gp("discover_exact").argtypes = [_p, _p, _u64, _u64, _u64, _u64, _u32, _f32, _f32, _p,
+                                             _p, _p]
         if pre == "or_":
             gp("discover").argtypes = [_p, _p, _u64, _u64, _u64, _u64, _u64, _u32, _f32, _f32, _p,
                                        _p, _p]
@@ -148,6 +160,42 @@ class Oracle:
                     rc = self._fn("discover")(_ptr(qs), _ptr(ks), 1, 1, L, d, B, tau, eps,
                                               _ptr(e1), _ptr(l1), _ptr(s1))
                     self._check(rc, "discover")
+                    en[z, h], lm[z, h], sc[z, h] = e1, l1, s1
+        return en, lm, sc
+
+    def sort_select(self, score, mode, param, B=128, sink_tokens=256, window_tokens=512):
+        """topk_select (mode 'topk', param k) / topp_select (mode 'topp', param p)."""
+        score = _f(score)
+        Z, H, M, _ = score.shape
+        mask = np.empty((Z, M, M, H), np.uint8)
+        fn = self._fn("topk_select" if mode == "topk" else "topp_select")
+        rc = fn(_ptr(score), Z, H, M, param, B, sink_tokens, window_tokens, _ptr(mask))
+        self._check(rc, mode)
+        return mask
+
+    def discover_variant(self, method, q, k, B, tau, eps=1e-10):
+        """discover_pool_both (method 'pool-both') / discover_exact (method 'exact')."""
+        q, k = _f(q), _f(k)
+        Z, Hq, L, d = q.shape
+        Hkv = k.shape[1]
+        M, _ = self.grid(L, B)
+        en = np.empty((Z, Hq, M, M), np.float32)
+        lm, sc = np.empty_like(en), np.empty_like(en)
+        name = "discover_pool_both" if method == "pool-both" else "discover_exact"
+        if self.kind == "port":
+            rc = self._fn(name)(_ptr(q), _ptr(k), Z, Hq, Hkv, L, d, B, tau, eps, _ptr(en), _ptr(lm),
+                                _ptr(sc))
+            self._check(rc, name)
+        else:
+            g = Hq // Hkv
+            for z in range(Z):
+                for h in range(Hq):
+                    qs = np.ascontiguousarray(q[z, h])
+                    ks = np.ascontiguousarray(k[z, h // g])
+                    e1, l1, s1 = (np.empty((M, M), np.float32) for _ in range(3))
+                    rc = self._fn(name)(_ptr(qs), _ptr(ks), 1, 1, L, d, B, tau, eps, _ptr(e1),
+                                        _ptr(l1), _ptr(s1))
+                    self._check(rc, name)
                     en[z, h], lm[z, h], sc[z, h] = e1, l1, s1
         return en, lm, sc
 

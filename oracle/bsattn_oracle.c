@@ -373,6 +373,182 @@ int or_full_causal_plan(uint64_t Z, uint64_t H, uint32_t M, int32_t* idx, int32_
 }
 
 /* ------------------------------------------------------------------------------------------
+ * Comparison baselines.  std::stable_sort(order, row[a] > row[b]) == sort by (score desc,
+ * index asc); restated with qsort on (score, index) pairs. */
+typedef struct {
+  float s;
+  uint32_t j;
+} or_pair;
+
+static int pair_cmp(const void* a, const void* b) {
+  const or_pair* x = (const or_pair*)a;
+  const or_pair* y = (const or_pair*)b;
+  if (x->s > y->s) return -1;
+  if (y->s > x->s) return 1;
+  return (x->j < y->j) ? -1 : (x->j > y->j);
+}
+
+static int sort_select(const float* score, uint64_t Z, uint64_t H, uint32_t M, int mode,
+                       uint32_t k, float p, uint32_t B, uint32_t sink_tokens,
+                       uint32_t window_tokens, uint8_t* mask) {
+  if (B < 1 || window_tokens < 1) return OR_EVALIDATION; /* PipelineConfig::validate */
+  if (mode == 0 && k < 1) return OR_EVALIDATION;         /* selection.hpp:98 */
+  if (mode == 1 && (!(p > 0.0f) || p > 1.0f)) return OR_EVALIDATION; /* selection.hpp:128 */
+  const uint32_t sink = (sink_tokens + B - 1) / B, window = (window_tokens + B - 1) / B;
+  const uint32_t N = M;
+  or_pair* order = (or_pair*)malloc(sizeof(or_pair) * M);
+  memset(mask, 0, Z * M * N * H);
+  for (uint64_t z = 0; z < Z; ++z)
+    for (uint64_t h = 0; h < H; ++h) {
+      const float* srow = score + (z * H + h) * M * N;
+      for (uint32_t i = 0; i < M; ++i) {
+        const float* row = srow + (uint64_t)i * N;
+        for (uint32_t j = 0; j <= i; ++j) {
+          order[j].s = row[j];
+          order[j].j = j;
+        }
+        qsort(order, i + 1, sizeof(or_pair), pair_cmp);
+        if (mode == 0) { /* selection.hpp:114-115 */
+          const uint32_t take = k < i + 1 ? k : i + 1;
+          for (uint32_t r = 0; r < take; ++r) mask[((z * M + i) * N + order[r].j) * H + h] = 1;
+        } else { /* selection.hpp:144-152 */
+          double total = 0.0;
+          for (uint32_t j = 0; j <= i; ++j) total += row[j];
+          double cumulative = 0.0;
+          for (uint32_t r = 0; r <= i; ++r) {
+            if (total <= 0.0 || order[r].s <= 0.0f) break;
+            mask[((z * M + i) * N + order[r].j) * H + h] = 1;
+            cumulative += order[r].s / total;
+            if (cumulative >= (double)p - 1e-9) break;
+          }
+        }
+        for (uint32_t j = 0; j <= i; ++j)
+          if (j < sink || (i - j) < window) mask[((z * M + i) * N + j) * H + h] = 1;
+      }
+    }
+  free(order);
+  return OR_OK;
+}
+
+int or_topk_select(const float* score, uint64_t Z, uint64_t H, uint32_t M, uint32_t k,
+                   uint32_t block_size, uint32_t sink_tokens, uint32_t window_tokens,
+                   uint8_t* mask) {
+  return sort_select(score, Z, H, M, 0, k, 0.f, block_size, sink_tokens, window_tokens, mask);
+}
+
+int or_topp_select(const float* score, uint64_t Z, uint64_t H, uint32_t M, float p,
+                   uint32_t block_size, uint32_t sink_tokens, uint32_t window_tokens,
+                   uint8_t* mask) {
+  return sort_select(score, Z, H, M, 1, 1, p, block_size, sink_tokens, window_tokens, mask);
+}
+
+/* discovery.hpp:164-195 */
+int or_discover_pool_both(const float* q, const float* k, uint64_t Z, uint64_t Hq, uint64_t Hkv,
+                          uint64_t L, uint64_t d, uint32_t B, float tau, float eps, float* energy,
+                          float* local_max, float* score) {
+  or_grid g;
+  if (or_make_grid(L, B, &g) || Hkv == 0 || Hq % Hkv) return OR_EVALIDATION;
+  const uint32_t M = g.num_blocks, N = M;
+  const uint64_t group = Hq / Hkv;
+  const float to_bits = tau * OR_LOG2E;
+  float* pq = (float*)malloc(sizeof(float) * Z * Hq * M * d);
+  float* pk = (float*)malloc(sizeof(float) * Z * Hkv * M * d);
+  or_pool_keys(q, Z, Hq, L, d, B, pq); /* detail::pool_blocks on the queries */
+  or_pool_keys(k, Z, Hkv, L, d, B, pk);
+  for (uint64_t i = 0; i < Z * Hq * M * N; ++i) {
+    energy[i] = 0.0f;
+    local_max[i] = NEG_SENTINEL;
+  }
+  for (uint64_t z = 0; z < Z; ++z)
+    for (uint64_t h = 0; h < Hq; ++h) {
+      const float* qb = pq + (z * Hq + h) * M * d;
+      const float* kb = pk + (z * Hkv + h / group) * N * d;
+      float* en = energy + (z * Hq + h) * M * N;
+      float* lm = local_max + (z * Hq + h) * M * N;
+      for (uint32_t qi = 0; qi < M; ++qi)
+        for (uint32_t kj = 0; kj <= qi; ++kj) {
+          lm[(uint64_t)qi * N + kj] =
+              or_dot_f32(qb + (uint64_t)qi * d, kb + (uint64_t)kj * d, d) * to_bits;
+          en[(uint64_t)qi * N + kj] = 1.0f;
+        }
+    }
+  free(pq);
+  free(pk);
+  return or_normalize_block_scores(energy, local_max, Z, Hq, M, eps, score);
+}
+
+/* discovery.hpp:201-279 */
+int or_discover_exact(const float* q, const float* k, uint64_t Z, uint64_t Hq, uint64_t Hkv,
+                      uint64_t L, uint64_t d, uint32_t B, float tau, float eps, float* energy,
+                      float* local_max, float* score) {
+  or_grid g;
+  if (or_make_grid(L, B, &g) || Hkv == 0 || Hq % Hkv) return OR_EVALIDATION;
+  const uint32_t M = g.num_blocks, N = M;
+  const uint64_t group = Hq / Hkv;
+  const float to_bits = tau * OR_LOG2E;
+  float* pk = (float*)malloc(sizeof(float) * Z * Hkv * N * d);
+  or_pool_keys(k, Z, Hkv, L, d, B, pk);
+  float* table = (float*)malloc(sizeof(float) * L * N);
+  for (uint64_t i = 0; i < Z * Hq * M * N; ++i) {
+    energy[i] = 0.0f;
+    local_max[i] = NEG_SENTINEL;
+    score[i] = 0.0f;
+  }
+  for (uint64_t z = 0; z < Z; ++z)
+    for (uint64_t h = 0; h < Hq; ++h) {
+      const float* qbase = q + (z * Hq + h) * L * d;
+      const float* kbase = pk + (z * Hkv + h / group) * N * d;
+      for (uint64_t t = 0; t < L; ++t) { /* pass 1: discovery.hpp:222-229 */
+        const uint32_t visible = (uint32_t)(t / B);
+        float* row = table + t * N;
+        for (uint32_t kj = 0; kj < N; ++kj)
+          row[kj] = kj <= visible ? or_dot_f32(qbase + t * d, kbase + (uint64_t)kj * d, d) * to_bits
+                                  : NEG_SENTINEL;
+      }
+      float* en = energy + (z * Hq + h) * M * N;
+      float* lm = local_max + (z * Hq + h) * M * N;
+      for (uint32_t qi = 0; qi < M; ++qi) { /* discovery.hpp:235-248 */
+        const uint32_t rows = block_len(&g, qi);
+        for (uint32_t kj = 0; kj <= qi; ++kj) {
+          float m = NEG_SENTINEL;
+          for (uint32_t r = 0; r < rows; ++r)
+            m = fmaxf_ref(m, table[((uint64_t)qi * B + r) * N + kj]);
+          float s = 0.0f;
+          for (uint32_t r = 0; r < rows; ++r) s += exp2f(table[((uint64_t)qi * B + r) * N + kj] - m);
+          lm[(uint64_t)qi * N + kj] = m;
+          en[(uint64_t)qi * N + kj] = s;
+        }
+      }
+      for (uint64_t t = 0; t < L; ++t) { /* pass 2: discovery.hpp:251-263 */
+        const uint32_t visible = (uint32_t)(t / B);
+        float* row = table + t * N;
+        float m = NEG_SENTINEL;
+        for (uint32_t kj = 0; kj <= visible; ++kj) m = fmaxf_ref(m, row[kj]);
+        float total = 0.0f;
+        for (uint32_t kj = 0; kj <= visible; ++kj) {
+          row[kj] = exp2f(row[kj] - m);
+          total += row[kj];
+        }
+        const float inv = 1.0f / (total + eps);
+        for (uint32_t kj = 0; kj <= visible; ++kj) row[kj] *= inv;
+      }
+      float* dst = score + (z * Hq + h) * M * N;
+      for (uint32_t qi = 0; qi < M; ++qi) { /* discovery.hpp:265-274 */
+        const uint32_t rows = block_len(&g, qi);
+        const float inv_rows = 1.0f / (float)rows;
+        for (uint32_t kj = 0; kj <= qi; ++kj) {
+          float acc = 0.0f;
+          for (uint32_t r = 0; r < rows; ++r) acc += table[((uint64_t)qi * B + r) * N + kj];
+          dst[(uint64_t)qi * N + kj] = acc * inv_rows;
+        }
+      }
+    }
+  free(pk);
+  free(table);
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------------------------
  * CPU baseline: the whole pipeline per (z, h) slice, slices spread over POSIX threads.
  * Per-slice calls are bit-identical to the batched reference call.           */
 typedef struct {

@@ -71,6 +71,20 @@ int or_dense_attention(const float* q, const float* k, const float* v, uint64_t 
 int or_full_causal_plan(uint64_t Z, uint64_t H, uint32_t M, int32_t* idx,
                         int32_t* counts);                                       /* attention.hpp:178-192 */
 
+/* Comparison baselines (not on the FlashPrefill path): selection.hpp:96-159, discovery.hpp:164-279 */
+int or_topk_select(const float* score, uint64_t Z, uint64_t H, uint32_t M, uint32_t k,
+                   uint32_t block_size, uint32_t sink_tokens, uint32_t window_tokens,
+                   uint8_t* mask);
+int or_topp_select(const float* score, uint64_t Z, uint64_t H, uint32_t M, float p,
+                   uint32_t block_size, uint32_t sink_tokens, uint32_t window_tokens,
+                   uint8_t* mask);
+int or_discover_pool_both(const float* q, const float* k, uint64_t Z, uint64_t Hq, uint64_t Hkv,
+                          uint64_t L, uint64_t d, uint32_t B, float tau, float eps, float* energy,
+                          float* local_max, float* score);
+int or_discover_exact(const float* q, const float* k, uint64_t Z, uint64_t Hq, uint64_t Hkv,
+                      uint64_t L, uint64_t d, uint32_t B, float tau, float eps, float* energy,
+                      float* local_max, float* score);
+
 /* Head-parallel pipeline used as the CPU baseline: discover -> mask -> compress -> sparse attn
  * for the given (z, h) slices on `threads` POSIX threads.  Returns wall seconds. */
 double or_pipeline_threads(const float* q, const float* k, const float* v, uint64_t Z, uint64_t Hq,

@@ -92,6 +92,60 @@ int ref_max_threshold_mask(const float* score, uint64_t Z, uint64_t H, uint32_t 
   });
 }
 
+int ref_topk_select(const float* score, uint64_t Z, uint64_t H, uint32_t M, uint32_t k,
+                    uint32_t block_size, uint32_t sink_tokens, uint32_t window_tokens,
+                    uint8_t* mask) {
+  return guarded([&] {
+    PipelineConfig cfg;
+    cfg.block_size = block_size;
+    cfg.sink_tokens = sink_tokens;
+    cfg.window_tokens = window_tokens;
+    const auto m = topk_select(make4(score, Z, H, M, M), k, cfg);
+    std::memcpy(mask, m.active.data(), m.active.numel());
+  });
+}
+
+int ref_topp_select(const float* score, uint64_t Z, uint64_t H, uint32_t M, float p,
+                    uint32_t block_size, uint32_t sink_tokens, uint32_t window_tokens,
+                    uint8_t* mask) {
+  return guarded([&] {
+    PipelineConfig cfg;
+    cfg.block_size = block_size;
+    cfg.sink_tokens = sink_tokens;
+    cfg.window_tokens = window_tokens;
+    const auto m = topp_select(make4(score, Z, H, M, M), p, cfg);
+    std::memcpy(mask, m.active.data(), m.active.numel());
+  });
+}
+
+static int ref_discover_variant(int which, const float* q, const float* k, uint64_t Z, uint64_t H,
+                                uint64_t L, uint64_t d, uint32_t B, float tau, float eps,
+                                float* energy, float* local_max, float* score) {
+  return guarded([&] {
+    const auto qb = batch(q, Z, H, L, d, Role::kQuery);
+    const auto kb = batch(k, Z, H, L, d, Role::kKey);
+    const auto grid = make_block_grid(L, B);
+    const auto map = which == 1 ? discover_pool_both(qb, kb, grid, tau, eps)
+                                : discover_exact(qb, kb, grid, tau, eps);
+    const size_t n = map.score.numel();
+    std::memcpy(energy, map.energy.data(), sizeof(float) * n);
+    std::memcpy(local_max, map.local_max.data(), sizeof(float) * n);
+    std::memcpy(score, map.score.data(), sizeof(float) * n);
+  });
+}
+
+int ref_discover_pool_both(const float* q, const float* k, uint64_t Z, uint64_t H, uint64_t L,
+                           uint64_t d, uint32_t B, float tau, float eps, float* energy,
+                           float* local_max, float* score) {
+  return ref_discover_variant(1, q, k, Z, H, L, d, B, tau, eps, energy, local_max, score);
+}
+
+int ref_discover_exact(const float* q, const float* k, uint64_t Z, uint64_t H, uint64_t L,
+                       uint64_t d, uint32_t B, float tau, float eps, float* energy,
+                       float* local_max, float* score) {
+  return ref_discover_variant(2, q, k, Z, H, L, d, B, tau, eps, energy, local_max, score);
+}
+
 int ref_compress_indices(const uint8_t* mask, uint64_t Z, uint32_t M, uint32_t N, uint64_t H,
                          int32_t* idx, int32_t* counts) {
   return guarded([&] {

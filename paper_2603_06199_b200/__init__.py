@@ -8,7 +8,8 @@ from .bsattn import (  # noqa: F401
     ActiveMask, AttentionOutput, AttentionStats, BlockEnergies, BlockGrid, BlockScoreMap,
     ConfigError, CudaError, FormatError, IoError, PipelineConfig, PlanError, PooledKeys,
     SelectionStats, SparseBlockPlan, ValidationError, approx_block_scores, block_sparse_attention,
-    compress_indices, dense_attention, density, discover, discover_select, flops_dense_causal,
+    compress_indices, dense_attention, density, discover, discover_exact, discover_pool_both,
+    discover_select, flops_dense_causal, topk_select, topp_select,
     flops_sparse, full_causal_plan, make_block_grid, make_sequence_batch, max_threshold_mask,
     normalize_block_scores, pool_keys, prefill, prefill_host, visit_count,
 )

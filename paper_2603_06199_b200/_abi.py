@@ -20,8 +20,11 @@ EXPORTS = [
     "fpb_pool_keys", "fpb_approx_block_scores", "fpb_normalize_block_scores", "fpb_discover",
     "fpb_max_threshold_mask", "fpb_compress_indices", "fpb_discover_select", "fpb_visit_count",
     "fpb_block_sparse_attention", "fpb_dense_attention", "fpb_full_causal_plan",
+    "fpb_topk_select", "fpb_topp_select", "fpb_baseline_workspace_bytes",
+    "fpb_discover_pool_both", "fpb_discover_exact",
     "fpb_host_pool_keys", "fpb_host_approx_block_scores", "fpb_host_normalize_block_scores",
     "fpb_host_discover", "fpb_host_max_threshold_mask", "fpb_host_compress_indices",
+    "fpb_host_topk_select", "fpb_host_topp_select", "fpb_host_discover_method",
     "fpb_host_block_sparse_attention", "fpb_host_dense_attention", "fpb_host_prefill",
 ]
 
@@ -70,6 +73,14 @@ def lib() -> C.CDLL:
             "fpb_dense_attention": (C.c_int, [P, C.c_int, p, p, p, C.c_int, p, p, p, C.c_size_t,
                                               p]),
             "fpb_full_causal_plan": (C.c_int, [P, p, p, p]),
+            "fpb_topk_select": (C.c_int, [P, p, C.c_int32, p, p]),
+            "fpb_topp_select": (C.c_int, [P, p, C.c_float, p, p]),
+            "fpb_baseline_workspace_bytes": (C.c_int, [P, C.POINTER(C.c_size_t)]),
+            "fpb_discover_pool_both": (C.c_int, [P, C.c_int, p, p, p, p, p, p, C.c_size_t, p]),
+            "fpb_discover_exact": (C.c_int, [P, C.c_int, p, p, p, p, p, p, C.c_size_t, p]),
+            "fpb_host_topk_select": (C.c_int, [P, p, C.c_int32, p]),
+            "fpb_host_topp_select": (C.c_int, [P, p, C.c_float, p]),
+            "fpb_host_discover_method": (C.c_int, [P, C.c_int, C.c_int, p, p, p, p, p]),
             "fpb_host_pool_keys": (C.c_int, [P, C.c_int, p, p]),
             "fpb_host_approx_block_scores": (C.c_int, [P, C.c_int, p, p, p, p]),
             "fpb_host_normalize_block_scores": (C.c_int, [P, p, p, p]),

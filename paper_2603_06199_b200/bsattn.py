@@ -364,6 +364,68 @@ def compress_indices(mask: ActiveMask) -> SparseBlockPlan:
     return SparseBlockPlan(idx, counts)
 
 
+def _sort_select(scores, config: PipelineConfig, mode: int, k: int = 1, p: float = 1.0):
+    config.validate()
+    score = scores.score if isinstance(scores, BlockScoreMap) else scores
+    _dev(score, "score")
+    Z, H, M, N = score.shape
+    pr = problem((Z, H, (M - 1) * config.block_size + 1, 128), H, config=config)
+    mask = torch.empty((Z, M, N, H), dtype=torch.uint8, device=score.device)
+    fn = _abi.lib().fpb_topk_select if mode == 0 else _abi.lib().fpb_topp_select
+    arg = C.c_int32(k) if mode == 0 else C.c_float(p)
+    rc = fn(C.byref(pr), _ptr(score), arg, _ptr(mask), _stream(score))
+    if rc == _abi.FPB_EVALIDATION:
+        raise ConfigError(_abi.last_error())
+    _raise(rc, "topk_select" if mode == 0 else "topp_select")
+    return ActiveMask(mask)
+
+
+def topk_select(scores, k: int, config: PipelineConfig) -> ActiveMask:
+    """selection.hpp:96-123 (comparison baseline): min(k, i+1) top blocks per causal row, ties
+    toward the lower index, plus sink/window retention."""
+    if k < 1:
+        raise ConfigError("top-k requires k >= 1")
+    return _sort_select(scores, config, 0, k=k)
+
+
+def topp_select(scores, p: float, config: PipelineConfig) -> ActiveMask:
+    """selection.hpp:127-159 (comparison baseline): shortest descending prefix reaching mass p."""
+    if not (p > 0.0) or p > 1.0:
+        raise ConfigError("top-p requires p in (0, 1]")
+    return _sort_select(scores, config, 1, p=p)
+
+
+def _baseline_discover(fn, name, queries, keys, grid, tau, epsilon):
+    _check_qk(queries, keys)
+    Z, Hq, L, d = queries.shape
+    M = grid.num_query_blocks
+    pr = problem(queries.shape, keys.shape[1], tau=tau, eps=epsilon)
+    pr.block_size = grid.block_size
+    n = C.c_size_t(0)
+    _raise(_abi.lib().fpb_baseline_workspace_bytes(C.byref(pr), C.byref(n)), name)
+    ws = torch.empty(max(1, n.value), dtype=torch.uint8, device=queries.device)
+    en = torch.empty((Z, Hq, M, M), dtype=torch.float32, device=queries.device)
+    lm, sc = torch.empty_like(en), torch.empty_like(en)
+    _raise(fn(C.byref(pr), _dtype_code(queries), _ptr(queries), _ptr(keys), _ptr(en), _ptr(lm),
+              _ptr(sc), _ptr(ws), n.value, _stream(queries)), name)
+    return BlockScoreMap(en, lm, sc)
+
+
+def discover_pool_both(queries, keys, grid: BlockGrid, tau: float,
+                       epsilon: float = kDefaultEpsilon) -> BlockScoreMap:
+    """discovery.hpp:164-195 (comparison method): mean-pool Q as well."""
+    return _baseline_discover(_abi.lib().fpb_discover_pool_both, "discover_pool_both", queries,
+                              keys, grid, tau, epsilon)
+
+
+def discover_exact(queries, keys, grid: BlockGrid, tau: float,
+                   epsilon: float = kDefaultEpsilon) -> BlockScoreMap:
+    """discovery.hpp:201-279 (reference semantics): per-query softmax over pooled keys, averaged
+    over each query block."""
+    return _baseline_discover(_abi.lib().fpb_discover_exact, "discover_exact", queries, keys,
+                              grid, tau, epsilon)
+
+
 def visit_count(plan: SparseBlockPlan) -> int:
     """selection.hpp:195-200."""
     c = _dev(plan.counts, "counts")
@@ -476,6 +538,7 @@ def full_causal_plan(batch: int, heads: int, grid: BlockGrid, device="cuda") -> 
     """attention.hpp:178-192."""
     M = grid.num_query_blocks
     p = problem((batch, heads, (M - 1) * grid.block_size + 1, 128), heads)
+    p.block_size = grid.block_size
     idx = torch.empty((batch, M, M, heads), dtype=torch.int32, device=device)
     counts = torch.empty((batch, M, heads), dtype=torch.int32, device=device)
     _raise(_abi.lib().fpb_full_causal_plan(C.byref(p), _ptr(idx), _ptr(counts),

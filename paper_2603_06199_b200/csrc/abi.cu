@@ -78,40 +78,51 @@ int resolve(const fpb_problem* p, Dims* D) {
   if (p->window_tokens < 1) return fail(FPB_EVALIDATION, "window_tokens must be >= 1");
   if (p->sink_tokens < 0) return fail(FPB_EVALIDATION, "sink_tokens must be >= 0");
   if (!(p->epsilon > 0.0f)) return fail(FPB_EVALIDATION, "epsilon must be > 0");
-  if (p->d != kHeadDim) return fail(FPB_EVALIDATION, "head_dim %lld unsupported (must be 128)", (long long)p->d);
-  if (p->block_size != kBlock)
-    return fail(FPB_EVALIDATION, "block_size %d unsupported (must be 128)", p->block_size);
-  if (p->L > (int64_t)1 << 30 || p->Z * p->Hq > (int64_t)1 << 24)
+  if (p->d > 1024) return fail(FPB_EVALIDATION, "head_dim %lld too large (max 1024)", (long long)p->d);
+  if (p->block_size > 4096)
+    return fail(FPB_EVALIDATION, "block_size %d too large (max 4096)", p->block_size);
+  if (p->L > (int64_t)1 << 30 || p->Z * p->Hq > (int64_t)1 << 24 ||
+      (p->L + p->block_size - 1) / p->block_size > 65535)
     return fail(FPB_EVALIDATION, "problem too large");
   D->Z = (int)p->Z;
   D->Hq = (int)p->Hq;
   D->Hkv = (int)p->Hkv;
   D->L = (int)p->L;
-  D->M = (int)((p->L + kBlock - 1) / kBlock);
+  D->B = p->block_size;
+  D->d = (int)p->d;
+  D->M = (int)((p->L + D->B - 1) / D->B);
   D->group = D->Hq / D->Hkv;
-  D->last_len = (int)(p->L - (int64_t)(D->M - 1) * kBlock);
+  D->last_len = (int)(p->L - (int64_t)(D->M - 1) * D->B);
   const float tau = p->scale > 0.0f ? p->scale : 1.0f / sqrtf((float)p->d);  // core.hpp:109-111
   D->to_bits = tau * kLog2e;
   D->eps = p->epsilon;
   D->alpha = p->alpha;
-  D->sink_blocks = (p->sink_tokens + kBlock - 1) / kBlock;      // core.hpp:103-105
-  D->window_blocks = (p->window_tokens + kBlock - 1) / kBlock;  // core.hpp:106-108
+  D->sink_blocks = (p->sink_tokens + D->B - 1) / D->B;      // core.hpp:103-105
+  D->window_blocks = (p->window_tokens + D->B - 1) / D->B;  // core.hpp:106-108
   return FPB_OK;
 }
+
+// The tcgen05/TMA kernels cover the tile shape d = B = 128; every other shape the reference
+// accepts runs the SIMT kernels of generic.cu.
+bool tc_path(const Dims& D) { return D.d == kHeadDim && D.B == kBlock; }
 
 int check_dtype(fpb_dtype t) {
   return (t == FPB_F32 || t == FPB_BF16) ? FPB_OK : fail(FPB_EUSAGE, "bad dtype %d", (int)t);
 }
 
-size_t q_elems(const Dims& D) { return (size_t)D.Z * D.Hq * D.L * kHeadDim; }
-size_t kv_elems(const Dims& D) { return (size_t)D.Z * D.Hkv * D.L * kHeadDim; }
+size_t q_elems(const Dims& D) { return (size_t)D.Z * D.Hq * D.L * D.d; }
+size_t kv_elems(const Dims& D) { return (size_t)D.Z * D.Hkv * D.L * D.d; }
 size_t map_elems(const Dims& D) { return (size_t)D.Z * D.Hq * D.M * D.M; }
+size_t pooled_bytes(const Dims& D) { return (size_t)D.Z * D.Hkv * D.M * D.d * 4; }
 size_t kbar_split_bytes(const Dims& D) { return 2ull * D.Z * D.Hkv * D.M * kHeadDim * 2; }
 
 // Workspace layouts.  discover: [scheduler counter][kbar split][Q hi/lo planes if fp32]
 //                     attention: [Q hi/lo][K hi/lo][V bf16] if fp32
+//   generic discover: [pooled][energy][local_max][score][mask]
 constexpr size_t kSchedBytes = 1024;
 size_t ws_discover(const Dims& D, fpb_dtype t) {
+  if (!tc_path(D))
+    return align_up(pooled_bytes(D)) + 3 * align_up(map_elems(D) * 4) + align_up(map_elems(D));
   size_t b = kSchedBytes + align_up(kbar_split_bytes(D));
   if (t == FPB_F32) b += align_up(2 * q_elems(D) * 2);
   return b;
@@ -128,6 +139,7 @@ DiscWs disc_ws(const Dims& D, void* ws) {
 }
 // attention: [sched][plan-row scratch] + fp32: Q hi/lo, K hi/lo, V bf16
 size_t ws_attention(const Dims& D, fpb_dtype t) {
+  if (!tc_path(D)) return align_up(g_attention_scratch_bytes(D));
   return kSchedBytes + align_up(attention_list_bytes(D)) +
          (t == FPB_F32 ? align_up(2 * q_elems(D) * 2) + align_up(2 * kv_elems(D) * 2) +
                              align_up(kv_elems(D) * 2)
@@ -210,7 +222,10 @@ int fpb_pool_keys(const fpb_problem* p, fpb_dtype dtype, const void* K, float* p
   int rc = resolve(p, &D);
   if (rc || (rc = check_dtype(dtype))) return rc;
   if (!K || !pooled) return fail(FPB_EUSAGE, "null pointer");
-  FPB_CUDA(launch_pool_keys(D, dtype == FPB_BF16, K, pooled, nullptr, S(stream)));
+  if (tc_path(D))
+    FPB_CUDA(launch_pool_keys(D, dtype == FPB_BF16, K, pooled, nullptr, S(stream)));
+  else
+    FPB_CUDA(g_launch_pool(D, dtype == FPB_BF16, K, pooled, S(stream)));
   return FPB_OK;
 }
 
@@ -221,6 +236,10 @@ int fpb_approx_block_scores(const fpb_problem* p, fpb_dtype dtype, const void* Q
   int rc = resolve(p, &D);
   if (rc || (rc = check_dtype(dtype))) return rc;
   if (!Q || !pooled || !energy || !local_max) return fail(FPB_EUSAGE, "null pointer");
+  if (!tc_path(D)) {
+    FPB_CUDA(g_launch_approx(D, dtype == FPB_BF16, Q, pooled, energy, local_max, S(stream)));
+    return FPB_OK;
+  }
   if ((rc = need_ws(workspace_bytes, ws_discover(D, dtype), workspace))) return rc;
   const DiscWs w = disc_ws(D, workspace);
   FPB_CUDA(launch_split_pooled(D, pooled, w.kbar, S(stream)));
@@ -258,6 +277,27 @@ int fpb_discover_select(const fpb_problem* p, fpb_dtype dtype, const void* Q, co
   if ((idx == nullptr) != (counts == nullptr))
     return fail(FPB_EUSAGE, "idx and counts must be given together");
   if ((rc = need_ws(workspace_bytes, ws_discover(D, dtype), workspace))) return rc;
+  if (!tc_path(D)) {  // pool -> approx -> normalize -> threshold -> compress, SIMT kernels
+    uint8_t* w = static_cast<uint8_t*>(workspace);
+    const size_t mb = align_up(map_elems(D) * 4);
+    float* pooled = reinterpret_cast<float*>(w);
+    float* en = reinterpret_cast<float*>(w + align_up(pooled_bytes(D)));
+    float* lm = reinterpret_cast<float*>(w + align_up(pooled_bytes(D)) + mb);
+    float* sc = reinterpret_cast<float*>(w + align_up(pooled_bytes(D)) + 2 * mb);
+    uint8_t* mk = w + align_up(pooled_bytes(D)) + 3 * mb;
+    en = energy ? energy : en;
+    lm = local_max ? local_max : lm;
+    sc = score ? score : sc;
+    mk = mask ? mask : mk;
+    FPB_CUDA(g_launch_pool(D, dtype == FPB_BF16, K, pooled, S(stream)));
+    FPB_CUDA(g_launch_approx(D, dtype == FPB_BF16, Q, pooled, en, lm, S(stream)));
+    FPB_CUDA(launch_normalize(D, en, lm, sc, S(stream)));
+    if (idx || mask) {
+      FPB_CUDA(launch_threshold(D, sc, mk, nullptr, S(stream)));
+      if (idx) FPB_CUDA(launch_compress(D, mk, idx, counts, S(stream)));
+    }
+    return FPB_OK;
+  }
   const DiscWs w = disc_ws(D, workspace);
   const __nv_bfloat16* qp;
   if ((rc = discover_prepare(D, dtype, Q, K, nullptr, w, S(stream), &qp))) return rc;
@@ -278,6 +318,78 @@ int fpb_discover(const fpb_problem* p, fpb_dtype dtype, const void* Q, const voi
   if (!score) return fail(FPB_EUSAGE, "null score");
   return fpb_discover_select(p, dtype, Q, K, energy, local_max, score, nullptr, nullptr, nullptr,
                              workspace, workspace_bytes, stream);
+}
+
+static int sort_select(const fpb_problem* p, const float* score, int mode, int32_t k,
+                       float top_p, uint8_t* mask, void* stream) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc) return rc;
+  if (!score || !mask) return fail(FPB_EUSAGE, "null pointer");
+  if (mode == 0 && k < 1) return fail(FPB_EVALIDATION, "top-k requires k >= 1");
+  if (mode == 1 && (!(top_p > 0.0f) || top_p > 1.0f))
+    return fail(FPB_EVALIDATION, "top-p requires p in (0, 1]");
+  if (D.M > 4096) return fail(FPB_EVALIDATION, "top-k/top-p rows limited to 4096 blocks");
+  FPB_CUDA(launch_sort_select(D, score, mask, mode, k, top_p, S(stream)));
+  return FPB_OK;
+}
+
+int fpb_topk_select(const fpb_problem* p, const float* score, int32_t k, uint8_t* mask,
+                    void* stream) {
+  return sort_select(p, score, 0, k, 0.f, mask, stream);
+}
+
+int fpb_topp_select(const fpb_problem* p, const float* score, float top_p, uint8_t* mask,
+                    void* stream) {
+  return sort_select(p, score, 1, 1, top_p, mask, stream);
+}
+
+int fpb_baseline_workspace_bytes(const fpb_problem* p, size_t* bytes) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc) return rc;
+  if (!bytes) return fail(FPB_EUSAGE, "null bytes");
+  const size_t pq = (size_t)D.Z * D.Hq * D.M * D.d * 4;
+  const size_t both = align_up(pq) + align_up(pooled_bytes(D));
+  const size_t exact = align_up(pooled_bytes(D)) + align_up(exact_table_bytes(D));
+  *bytes = both > exact ? both : exact;
+  return FPB_OK;
+}
+
+int fpb_discover_pool_both(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                           float* energy, float* local_max, float* score, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc || (rc = check_dtype(dtype))) return rc;
+  if (!Q || !K || !energy || !local_max || !score) return fail(FPB_EUSAGE, "null pointer");
+  size_t need;
+  fpb_baseline_workspace_bytes(p, &need);
+  if ((rc = need_ws(workspace_bytes, need, workspace))) return rc;
+  uint8_t* w = static_cast<uint8_t*>(workspace);
+  float* pq = reinterpret_cast<float*>(w);
+  float* pk = reinterpret_cast<float*>(w + align_up((size_t)D.Z * D.Hq * D.M * D.d * 4));
+  FPB_CUDA(launch_pool_both(D, dtype == FPB_BF16, Q, K, pq, pk, energy, local_max, S(stream)));
+  FPB_CUDA(launch_normalize(D, energy, local_max, score, S(stream)));
+  return FPB_OK;
+}
+
+int fpb_discover_exact(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                       float* energy, float* local_max, float* score, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc || (rc = check_dtype(dtype))) return rc;
+  if (!Q || !K || !energy || !local_max || !score) return fail(FPB_EUSAGE, "null pointer");
+  size_t need;
+  fpb_baseline_workspace_bytes(p, &need);
+  if ((rc = need_ws(workspace_bytes, need, workspace))) return rc;
+  uint8_t* w = static_cast<uint8_t*>(workspace);
+  float* pk = reinterpret_cast<float*>(w);
+  float* table = reinterpret_cast<float*>(w + align_up(pooled_bytes(D)));
+  FPB_CUDA(launch_exact(D, dtype == FPB_BF16, Q, K, pk, table, energy, local_max, score,
+                        S(stream)));
+  return FPB_OK;
 }
 
 int fpb_max_threshold_mask(const fpb_problem* p, const float* score, uint8_t* mask,
@@ -331,6 +443,12 @@ static int attention_common(const fpb_problem* p, fpb_dtype dtype, const void* Q
   if (rc || (rc = check_dtype(dtype)) || (rc = check_dtype(out_dtype))) return rc;
   if (!Q || !K || !V || !out || !lse) return fail(FPB_EUSAGE, "null pointer");
   if ((rc = need_ws(workspace_bytes, ws_attention(D, dtype), workspace))) return rc;
+  if (!tc_path(D)) {
+    FPB_CUDA(g_launch_attention(D, dtype == FPB_BF16, Q, K, V, idx, counts,
+                                out_dtype == FPB_BF16, out, lse, visits, plan_error,
+                                static_cast<float*>(workspace), S(stream)));
+    return FPB_OK;
+  }
   const __nv_bfloat16 *q = static_cast<const __nv_bfloat16*>(Q),
                       *k = static_cast<const __nv_bfloat16*>(K),
                       *v = static_cast<const __nv_bfloat16*>(V);
@@ -433,7 +551,7 @@ int fpb_host_pool_keys(const fpb_problem* p, fpb_dtype dtype, const void* K, flo
   int rc = resolve(p, &D);
   if (rc || (rc = check_dtype(dtype))) return rc;
   if (!K || !pooled) return fail(FPB_EUSAGE, "null pointer");
-  const size_t kb = kv_elems(D) * dsz(dtype), pb = (size_t)D.Z * D.Hkv * D.M * kHeadDim * 4;
+  const size_t kb = kv_elems(D) * dsz(dtype), pb = pooled_bytes(D);
   uint8_t* base;
   cudaStream_t st;
   if ((rc = arena_get(align_up(kb) + align_up(pb), &base, &st))) return rc;
@@ -453,7 +571,7 @@ int fpb_host_approx_block_scores(const fpb_problem* p, fpb_dtype dtype, const vo
   int rc = resolve(p, &D);
   if (rc || (rc = check_dtype(dtype))) return rc;
   if (!Q || !pooled || !energy || !local_max) return fail(FPB_EUSAGE, "null pointer");
-  const size_t qb = q_elems(D) * dsz(dtype), pb = (size_t)D.Z * D.Hkv * D.M * kHeadDim * 4,
+  const size_t qb = q_elems(D) * dsz(dtype), pb = pooled_bytes(D),
                mb = map_elems(D) * 4, wsb = ws_discover(D, dtype);
   uint8_t* base;
   cudaStream_t st;
@@ -549,6 +667,68 @@ int fpb_host_max_threshold_mask(const fpb_problem* p, const float* score, uint8_
   FPB_CUDA(cudaMemcpyAsync(&cmp, dc, 8, cudaMemcpyDeviceToHost, st));
   FPB_CUDA(cudaStreamSynchronize(st));
   if (comparisons) *comparisons += cmp;
+  return FPB_OK;
+}
+
+static int host_sort_select(const fpb_problem* p, const float* score, int mode, int32_t k,
+                            float top_p, uint8_t* mask) {
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc) return rc;
+  if (!score || !mask) return fail(FPB_EUSAGE, "null pointer");
+  const size_t sb = map_elems(D) * 4, mb = map_elems(D);
+  uint8_t* base;
+  cudaStream_t st;
+  if ((rc = arena_get(align_up(sb) + align_up(mb), &base, &st))) return rc;
+  Carve c{base};
+  float* ds = c.take<float>(sb);
+  uint8_t* dm = c.take<uint8_t>(mb);
+  FPB_CUDA(cudaMemcpyAsync(ds, score, sb, cudaMemcpyHostToDevice, st));
+  if ((rc = sort_select(p, ds, mode, k, top_p, dm, st))) return rc;
+  FPB_CUDA(cudaMemcpyAsync(mask, dm, mb, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaStreamSynchronize(st));
+  return FPB_OK;
+}
+
+int fpb_host_topk_select(const fpb_problem* p, const float* score, int32_t k, uint8_t* mask) {
+  return host_sort_select(p, score, 0, k, 0.f, mask);
+}
+
+int fpb_host_topp_select(const fpb_problem* p, const float* score, float top_p, uint8_t* mask) {
+  return host_sort_select(p, score, 1, 1, top_p, mask);
+}
+
+int fpb_host_discover_method(const fpb_problem* p, fpb_dtype dtype, int method, const void* Q,
+                             const void* K, float* energy, float* local_max, float* score) {
+  if (method == 0) return fpb_host_discover(p, dtype, Q, K, energy, local_max, score);
+  if (method != 1 && method != 2) return fail(FPB_EUSAGE, "unknown discovery method %d", method);
+  Dims D;
+  int rc = resolve(p, &D);
+  if (rc || (rc = check_dtype(dtype))) return rc;
+  if (!Q || !K || !energy || !local_max || !score) return fail(FPB_EUSAGE, "null pointer");
+  size_t wsb;
+  fpb_baseline_workspace_bytes(p, &wsb);
+  const size_t qb = q_elems(D) * dsz(dtype), kb = kv_elems(D) * dsz(dtype), mb = map_elems(D) * 4;
+  uint8_t* base;
+  cudaStream_t st;
+  if ((rc = arena_get(align_up(qb) + align_up(kb) + 3 * align_up(mb) + align_up(wsb), &base, &st)))
+    return rc;
+  Carve c{base};
+  void* dq = c.take<void>(qb);
+  void* dk = c.take<void>(kb);
+  float* de = c.take<float>(mb);
+  float* dl = c.take<float>(mb);
+  float* ds = c.take<float>(mb);
+  void* ws = c.take<void>(wsb);
+  FPB_CUDA(cudaMemcpyAsync(dq, Q, qb, cudaMemcpyHostToDevice, st));
+  FPB_CUDA(cudaMemcpyAsync(dk, K, kb, cudaMemcpyHostToDevice, st));
+  rc = method == 1 ? fpb_discover_pool_both(p, dtype, dq, dk, de, dl, ds, ws, wsb, st)
+                   : fpb_discover_exact(p, dtype, dq, dk, de, dl, ds, ws, wsb, st);
+  if (rc) return rc;
+  FPB_CUDA(cudaMemcpyAsync(energy, de, mb, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaMemcpyAsync(local_max, dl, mb, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaMemcpyAsync(score, ds, mb, cudaMemcpyDeviceToHost, st));
+  FPB_CUDA(cudaStreamSynchronize(st));
   return FPB_OK;
 }
 
@@ -660,7 +840,7 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
   int cq = group;
   while (cq % 2 == 0 && (int64_t)D.Z * D.Hq / cq < min_chunks) cq /= 2;
   const int chunks_per_z = D.Hq / cq, nch = D.Z * chunks_per_z;
-  const size_t es = dsz(dtype), eo = dsz(out_dtype), Ld = (size_t)D.L * kHeadDim;
+  const size_t es = dsz(dtype), eo = dsz(out_dtype), Ld = (size_t)D.L * D.d;
   const size_t qb = q_elems(D) * es, kb = kv_elems(D) * es, ob = q_elems(D) * eo,
                lb = (size_t)D.Z * D.Hq * D.L * 4;
   fpb_problem sub = *p;

@@ -21,10 +21,12 @@ struct Dims {
   float to_bits;            // tau * log2(e)
   float eps, alpha;
   int sink_blocks, window_blocks;
+  int B, d;                 // block size and head dim (128 / 128 on the tensor-core path)
 };
+using GenDims = Dims;
 
 __host__ __device__ __forceinline__ int block_len(const Dims& D, int blk) {
-  return blk + 1 == D.M ? D.last_len : kBlock;
+  return blk + 1 == D.M ? D.last_len : D.B;
 }
 
 // Block-wide reductions over `nthreads` (multiple of 32) threads using `scratch` (>= 32 floats).

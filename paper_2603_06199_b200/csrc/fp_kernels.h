@@ -54,6 +54,28 @@ cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __n
 // bytes of the compacted-plan scratch launch_attention needs (grid x 2 slots x 2 bufs x M x u16)
 size_t attention_list_bytes(const Dims& D);
 
+// generic.cu — SIMT kernels for shapes outside the tensor-core tile (d != 128 or B != 128)
+cudaError_t g_launch_pool(const GenDims& G, bool bf16_in, const void* K, float* pooled,
+                          cudaStream_t s);
+cudaError_t g_launch_approx(const GenDims& G, bool bf16_in, const void* Q, const float* pooled,
+                            float* energy, float* local_max, cudaStream_t s);
+size_t g_attention_scratch_bytes(const GenDims& G);
+cudaError_t g_launch_attention(const GenDims& G, bool bf16_in, const void* Q, const void* K,
+                               const void* V, const int32_t* idx, const int32_t* counts,
+                               bool out_bf16, void* out, float* lse, unsigned long long* visits,
+                               int32_t* plan_error, float* scratch, cudaStream_t s);
+
+// baselines.cu — comparison methods of the reference (top-k / top-p, pool-both, exact)
+cudaError_t launch_sort_select(const Dims& D, const float* score, uint8_t* mask, int mode, int k,
+                               float p, cudaStream_t s);  // mode 0: top-k, 1: top-p
+cudaError_t launch_pool_both(const Dims& D, bool bf16_in, const void* Q, const void* K,
+                             float* pooled_q, float* pooled_k, float* energy, float* local_max,
+                             cudaStream_t s);
+size_t exact_table_bytes(const Dims& D);
+cudaError_t launch_exact(const Dims& D, bool bf16_in, const void* Q, const void* K, float* pooled,
+                         float* table, float* energy, float* local_max, float* score,
+                         cudaStream_t s);
+
 // tensor maps (abi.cu)
 bool make_tmap_rows128(CUtensorMap* map, const void* base, uint64_t rows, uint64_t planes);
 

@@ -63,6 +63,13 @@ def main():
             if al == 0.12:
                 o, lse, vis = R.block_sparse_attention(q, k, v, idx, counts, B, tau)
                 out.update(out_sparse=o, lse_sparse=lse, visits=np.array([vis], np.uint64))
+        if not bf:  # comparison baselines (selection.hpp:94-159, discovery.hpp:161-279)
+            out["topk4"] = R.sort_select(sc, "topk", 4, B, 256, 512)
+            out["topp09"] = R.sort_select(sc, "topp", 0.9, B, 256, 512)
+            for method in ("pool-both", "exact"):
+                e2, l2, s2 = R.discover_variant(method, q, k, B, tau)
+                tag = method.replace("-", "_")
+                out.update({f"{tag}_energy": e2, f"{tag}_local_max": l2, f"{tag}_score": s2})
         if L <= 1100:
             o, lse = R.dense_attention(q, k, v, tau)
             out.update(out_dense=o, lse_dense=lse)

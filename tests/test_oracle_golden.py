@@ -51,6 +51,14 @@ def test_oracle_matches_reference_golden(port, path):
     if "out_dense" in g:
         o, lse = port.dense_attention(q, k, v, tau)
         assert np.array_equal(o, g["out_dense"]) and np.array_equal(lse, g["lse_dense"])
+    if "topk4" in g:  # comparison baselines
+        assert np.array_equal(port.sort_select(sc, "topk", 4, B, 256, 512), g["topk4"])
+        assert np.array_equal(port.sort_select(sc, "topp", 0.9, B, 256, 512), g["topp09"])
+        for name in ("pool-both", "exact"):
+            tag = name.replace("-", "_")
+            e2, l2, s2 = port.discover_variant(name, q, k, B, tau)
+            assert np.array_equal(e2, g[f"{tag}_energy"]) and np.array_equal(l2, g[f"{tag}_local_max"])
+            assert np.array_equal(s2, g[f"{tag}_score"])
 
 
 def test_oracle_matches_live_reference(port, ref):

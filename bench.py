@@ -47,6 +47,20 @@ def peaks():
         return {"hbm": 6650.0, "tc_burst": 1590.0, "tc_sustained": 1400.0, "src": "fallback"}
 
 
+def ncu_traffic(kernel: str, cfg: dict):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of `kernel` from the
+    committed `ncu --set full` capture (profiles/ncu_traffic.json, written by
+    tools/ncu_summary.py --traffic); None unless the capture was taken on this exact config."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            rec = json.load(f)[kernel]
+    except (OSError, KeyError, ValueError):
+        return None
+    if any(rec.get("config", {}).get(k) != v for k, v in cfg.items()):
+        return None
+    return rec["dram_bytes"]
+
+
 class ClockSampler:
     """SM clocks / throttle reasons sampled via NVML every ~2 ms DURING the timed region
     (nvidia-smi's 200 ms loop is too coarse for a ~20 ms region)."""
@@ -291,6 +305,8 @@ def run_gpu_arm(args, rank, world, dist):
     # discovery algorithmic bytes: read Q and K once, write idx (incl. fill) and counts
     disc_bytes = args.hq * args.L * D * 2 + args.hkv * args.L * D * 2 \
         + M * M * args.hq * 4 + M * args.hq * 4
+    traffic_cfg = {"L": args.L, "hq": args.hq, "hkv": args.hkv, "alpha": args.alpha,
+                   "seed": args.seed}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -309,9 +325,12 @@ def run_gpu_arm(args, rank, world, dist):
         "density": dens, "block_visits": visits, "diag_visits": diag,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": pk["tc_sustained"],
                      "unit": "TFLOP/s", "frac": achieved / pk["tc_sustained"],
-                     "frac_of_burst": achieved / pk["tc_burst"], "traffic": None,
-                     "kernel": "attention_kernel (K4)", "peak_src": pk["src"] + " sustained"},
-        "discovery_roofline": {"bound": "hbm", "achieved": disc_bytes / (ms_disc * 1e-3) / 1e9,
+                     "frac_of_burst": achieved / pk["tc_burst"],
+                     "traffic": ncu_traffic("fa_kernel", traffic_cfg),
+                     "traffic_unit": "bytes per launch (ncu --set full, cold L2)",
+                     "kernel": "fa_kernel (K4, csrc/attention_fa.cu)", "peak_src": pk["src"] + " sustained"},
+        "discovery_roofline": {"bound": "hbm", "kernel": "discover_kernel (K2+K3)",
+                               "traffic": ncu_traffic("discover_kernel", traffic_cfg), "achieved": disc_bytes / (ms_disc * 1e-3) / 1e9,
                                "peak": pk["hbm"], "unit": "GB/s",
                                "frac": disc_bytes / (ms_disc * 1e-3) / 1e9 / pk["hbm"],
                                "bytes": disc_bytes},

@@ -308,6 +308,42 @@ class Oracle:
             raise ValueError("pipeline failed")
         return secs, out, lse, vis.value
 
+    # ------------------------------------------------------------------ reference-only (CLI pins)
+    def _ref_only(self, name):
+        if self.kind != "reference":
+            raise NotImplementedError(f"{name}: reference shim only (pins the CLI restatement)")
+        return getattr(self.lib, "ref_" + name)
+
+    def generate_alternating_slash(self, strength, offset, noise, seed, Z, H, L, d, B, tau=0.0):
+        """workloads.hpp:269-311: returns (q, k, v, ground_truth Z x M x M x H)."""
+        f = self._ref_only("generate_alternating_slash")
+        f.argtypes = [_f32, _i64, _f32, _u64, _u64, _u64, _u64, _u64, _u32, _f32, _p, _p, _p, _p]
+        q = np.empty((Z, H, L, d), np.float32)
+        k, v = np.empty_like(q), np.empty_like(q)
+        M, _ = self.grid(L, B)
+        gt = np.empty((Z, M, M, H), np.uint8)
+        self._check(f(strength, offset, noise, seed, Z, H, L, d, B, tau, _ptr(q), _ptr(k), _ptr(v),
+                      _ptr(gt)), "generate_alternating_slash")
+        return q, k, v, gt
+
+    def heavy_tail_sweep_map(self, n, head_mass, alpha, seed):
+        """workloads.hpp:378-399: (score 1 x 1 x n x n, head_index[n])."""
+        f = self._ref_only("heavy_tail_sweep_map")
+        f.argtypes = [_u32, _f32, _f32, _u64, _p, _p]
+        score = np.empty((1, 1, n, n), np.float32)
+        head = np.empty(n, np.int32)
+        self._check(f(n, head_mass, alpha, seed, _ptr(score), _ptr(head)), "heavy_tail_sweep_map")
+        return score, head
+
+    def save_tensor(self, arr, path):
+        """tensor.hpp save_tensor (FPT1) for f32 / i32 arrays."""
+        arr = np.ascontiguousarray(arr)
+        name = "save_tensor_f32" if arr.dtype == np.float32 else "save_tensor_i32"
+        f = self._ref_only(name)
+        f.argtypes = [_p, _p, _i32, C.c_char_p]
+        shape = np.asarray(arr.shape, np.uint64)
+        self._check(f(_ptr(arr), _ptr(shape), arr.ndim, os.fsencode(path)), name)
+
     # ------------------------------------------------------------------ plain numpy helpers
     @staticmethod
     def visit_count(counts) -> int:

@@ -14,6 +14,7 @@
 #include "bsattn/attention.hpp"
 #include "bsattn/discovery.hpp"
 #include "bsattn/selection.hpp"
+#include "bsattn/tensor.hpp"
 #include "bsattn/workloads.hpp"
 
 using namespace bsattn;
@@ -207,6 +208,52 @@ int ref_generate_planted(int kind, float strength, int64_t target_a, int64_t tar
     std::memcpy(k, w.k.data.data(), sizeof(float) * n);
     std::memcpy(v, w.v.data.data(), sizeof(float) * n);
     if (gt) std::memcpy(gt, w.ground_truth.active.data(), w.ground_truth.active.numel());
+  });
+}
+
+// workloads.hpp:269-311 (pins the CLI's alt-slash generator, tools/cli/workloads.hpp)
+int ref_generate_alternating_slash(float strength, int64_t offset, float base_noise, uint64_t seed,
+                                   uint64_t Z, uint64_t H, uint64_t L, uint64_t d, uint32_t B,
+                                   float tau, float* q, float* k, float* v, uint8_t* gt) {
+  return guarded([&] {
+    PlantedSpec spec;
+    spec.pattern_kind = PatternKind::kSlash;
+    spec.strength = strength;
+    spec.target_a = offset;
+    spec.base_noise = base_noise;
+    spec.rng_seed = seed;
+    const auto w = generate_alternating_slash(spec, Z, H, L, d, B, tau);
+    const size_t n = w.q.data.numel();
+    std::memcpy(q, w.q.data.data(), sizeof(float) * n);
+    std::memcpy(k, w.k.data.data(), sizeof(float) * n);
+    std::memcpy(v, w.v.data.data(), sizeof(float) * n);
+    std::memcpy(gt, w.ground_truth.active.data(), w.ground_truth.active.numel());
+  });
+}
+
+// workloads.hpp:378-399: score n x n, head_index n
+int ref_heavy_tail_sweep_map(uint32_t n, float head_mass, float alpha, uint64_t seed, float* score,
+                             int32_t* head_index) {
+  return guarded([&] {
+    const auto m = heavy_tail_sweep_map(n, head_mass, alpha, seed);
+    std::memcpy(score, m.score.data(), sizeof(float) * m.score.numel());
+    std::memcpy(head_index, m.head_index.data(), sizeof(int32_t) * n);
+  });
+}
+
+// tensor.hpp save_tensor: the reference's FPT1 writer (pins the container bytes)
+int ref_save_tensor_f32(const float* data, const uint64_t* shape, int ndim, const char* path) {
+  return guarded([&] {
+    Tensor<float> t(std::vector<std::uint64_t>(shape, shape + ndim));
+    std::memcpy(t.data(), data, sizeof(float) * t.numel());
+    save_tensor(t, path);
+  });
+}
+int ref_save_tensor_i32(const int32_t* data, const uint64_t* shape, int ndim, const char* path) {
+  return guarded([&] {
+    Tensor<std::int32_t> t(std::vector<std::uint64_t>(shape, shape + ndim));
+    std::memcpy(t.data(), data, sizeof(int32_t) * t.numel());
+    save_tensor(t, path);
   });
 }
 

@@ -47,6 +47,33 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     return out
 
 
+ROOT = os.path.dirname(HERE)
+CLI = os.path.join(HERE, "fpb200_cli")
+CLI_SOURCES = [os.path.join(ROOT, "tools", "fpb200_cli.cpp"),
+               os.path.join(ROOT, "tools", "cli", "json.hpp"),
+               os.path.join(ROOT, "tools", "cli", "workloads.hpp"),
+               os.path.join(ROOT, "include", "fpb200", "bsattn.hpp"),
+               os.path.join(ROOT, "include", "fpb200", "fpt1.hpp"),
+               os.path.join(ROOT, "include", "fpb200.h")]
+
+
+def build_cli(force: bool = False) -> str:
+    """The reference-compatible CLI (tools/fpb200_cli.cpp) linked against libfpb200.so ($ORIGIN rpath)."""
+    build()
+    if (not force and os.path.exists(CLI)
+            and all(os.path.getmtime(p) <= os.path.getmtime(CLI) for p in CLI_SOURCES + [LIB])):
+        return CLI
+    cmd = [os.environ.get("CXX", "g++"), "-std=c++17", "-O2", "-Wall", "-Wextra",
+           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(ROOT, "tools"),
+           CLI_SOURCES[0], f"-L{HERE}", "-l:libfpb200.so", "-Wl,-rpath,$ORIGIN", "-o", CLI + ".tmp"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("g++ failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
+    os.replace(CLI + ".tmp", CLI)
+    return CLI
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)
+    print(build_cli(force="--force" in sys.argv))

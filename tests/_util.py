@@ -82,3 +82,30 @@ def composite_np(seed: int, Z: int, Hq: int, Hkv: int, L: int, d: int = 128, B: 
                     s = rng.uniform(0.5, 3.0)
                     q[z, hq] += (s / tau / np.sqrt(max(1, n_slash)) * dirs[tok]).astype(np.float32)
     return q, k, v
+
+
+# ------------------------------------------------------------------ FPT1 container (tensor.hpp:97-221)
+_FPT_DTYPES = {0: np.float32, 1: np.int32}
+
+
+def write_fpt(path, arr) -> None:
+    """Little-endian FPT1: magic, u32 version 1, u32 ndim, u64 dims, u32 dtype (0 f32 / 1 i32)."""
+    arr = np.ascontiguousarray(arr)
+    code = {np.dtype(np.float32): 0, np.dtype(np.int32): 1}[arr.dtype]
+    hdr = b"FPT1" + np.array([1, arr.ndim], "<u4").tobytes() + np.array(arr.shape, "<u8").tobytes()
+    with open(path, "wb") as f:
+        f.write(hdr + np.array([code], "<u4").tobytes() + arr.astype(arr.dtype.newbyteorder("<")).tobytes())
+
+
+def read_fpt(path) -> np.ndarray:
+    raw = open(path, "rb").read()
+    assert raw[:4] == b"FPT1", "bad magic"
+    version, ndim = np.frombuffer(raw, "<u4", 2, 4)
+    assert version == 1
+    shape = tuple(int(x) for x in np.frombuffer(raw, "<u8", int(ndim), 12))
+    off = 12 + 8 * int(ndim)
+    code = int(np.frombuffer(raw, "<u4", 1, off)[0])
+    n = int(np.prod(shape))
+    data = np.frombuffer(raw, np.dtype(_FPT_DTYPES[code]).newbyteorder("<"), n, off + 4)
+    assert off + 4 + 4 * n == len(raw), "trailing bytes"
+    return data.reshape(shape).astype(_FPT_DTYPES[code])

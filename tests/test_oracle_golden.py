@@ -12,7 +12,8 @@ import pytest
 
 from oracle import LOG2E, NEG_SENTINEL
 
-GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+GOLDEN = sorted(p for p in glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz"))
+                if os.path.basename(p) != "cli.npz")  # cli.npz: CLI fixtures, tests/test_cli.py
 
 
 def _inputs(port, P):

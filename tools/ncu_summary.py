@@ -2,7 +2,12 @@
 """Summarise an ncu --set full report (raw page) into the metrics the roofline argument needs.
 
 usage: python tools/ncu_summary.py gpurun_out/r1_attn.ncu-rep [more.ncu-rep ...]
+       python tools/ncu_summary.py --traffic KERNEL 'CONFIG_JSON' rep.ncu-rep
+           records that kernel's per-launch DRAM bytes (read + write) in profiles/ncu_traffic.json,
+           which bench.py reports as roofline.traffic when its config matches CONFIG_JSON.
 """
+import json
+import os
 import csv
 import io
 import subprocess
@@ -63,7 +68,35 @@ def summarise(path):
     return "\n".join(out) + "\n"
 
 
+_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def traffic(path, kernel, cfg):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    for r in rows[2:]:
+        if kernel not in r[hdr.index("Kernel Name")]:
+            continue
+        tot = 0.0
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(key)
+            tot += float(r[i].replace(",", "")) * _SCALE[units[i]]
+        dest = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "profiles", "ncu_traffic.json")
+        data = json.load(open(dest)) if os.path.exists(dest) else {}
+        data[kernel] = {"dram_bytes": tot, "config": cfg, "capture": os.path.basename(path)}
+        with open(dest, "w") as f:
+            json.dump(data, f, indent=1)
+        return tot
+    raise SystemExit(f"{kernel} not in {path}")
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "--traffic":
+        print(traffic(sys.argv[4], sys.argv[2], json.loads(sys.argv[3])))
+        sys.exit(0)
     for p in sys.argv[1:]:
         print(f"== {p}")
         print(summarise(p))

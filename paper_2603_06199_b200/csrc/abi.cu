@@ -879,6 +879,22 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
     FPB_CUDA(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming));
   }
   FPB_CUDA(cudaMemsetAsync(dvis, 0, 8 * nch, st));
+  // FPB_E2E_TRACE=1: per-chunk timeline (H2D done / kernels done / D2H done) on stderr
+  static const bool trace = getenv("FPB_E2E_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tr_in, tr_k, tr_out;
+  cudaEvent_t tr0 = nullptr;
+  auto tr_mark = [&](std::vector<cudaEvent_t>& v, cudaStream_t s) -> int {
+    if (!trace) return FPB_OK;
+    cudaEvent_t e;
+    FPB_CUDA(cudaEventCreate(&e));
+    FPB_CUDA(cudaEventRecord(e, s));
+    v.push_back(e);
+    return FPB_OK;
+  };
+  if (trace) {
+    FPB_CUDA(cudaEventCreate(&tr0));
+    FPB_CUDA(cudaEventRecord(tr0, s_in));
+  }
   const uint8_t* hq = static_cast<const uint8_t*>(Q);
   const uint8_t* hk = static_cast<const uint8_t*>(K);
   const uint8_t* hv = static_cast<const uint8_t*>(V);
@@ -892,6 +908,7 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
     const size_t off = ((size_t)z * D.Hq + q0) * Ld * es;
     FPB_CUDA(cudaMemcpyAsync(dq + off, hq + off, cq * Ld * es, cudaMemcpyHostToDevice, s_in));
     FPB_CUDA(cudaEventRecord(ev_in[i], s_in));
+    if ((rc = tr_mark(tr_in, s_in))) return rc;
   }
   for (int i = 0; i < nch; ++i) {  // kernels of each chunk on the compute stream
     const int z = i / chunks_per_z, q0 = (i % chunks_per_z) * cq, kv = q0 / group;
@@ -908,6 +925,7 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
                                          dvis + i, nullptr, ws, wsb, st)))
       return rc;
     FPB_CUDA(cudaEventRecord(ev_done[i], st));
+    if ((rc = tr_mark(tr_k, st))) return rc;
   }
   uint8_t* ho = static_cast<uint8_t*>(out);
   for (int i = 0; i < nch; ++i) {  // D2H of each finished chunk
@@ -927,11 +945,25 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
       FPB_CUDA(cudaMemcpy2DAsync(counts + (size_t)z * D.M * D.Hq + q0, (size_t)D.Hq * 4, dc[i],
                                  (size_t)cq * 4, (size_t)cq * 4, (size_t)D.M,
                                  cudaMemcpyDeviceToHost, s_out));
+    if ((rc = tr_mark(tr_out, s_out))) return rc;
   }
   std::vector<unsigned long long> vis(nch, 0);
   FPB_CUDA(cudaStreamSynchronize(st));
   FPB_CUDA(cudaMemcpyAsync(vis.data(), dvis, 8 * nch, cudaMemcpyDeviceToHost, s_out));
   FPB_CUDA(cudaStreamSynchronize(s_out));
+  if (trace) {
+    for (int i = 0; i < nch; ++i) {
+      float a = 0, b = 0, c2 = 0;
+      cudaEventElapsedTime(&a, tr0, tr_in[i]);
+      cudaEventElapsedTime(&b, tr0, tr_k[i]);
+      cudaEventElapsedTime(&c2, tr0, tr_out[i]);
+      fprintf(stderr, "e2e chunk %2d: h2d %.3f  kernels %.3f  d2h %.3f ms\n", i, a, b, c2);
+      cudaEventDestroy(tr_in[i]);
+      cudaEventDestroy(tr_k[i]);
+      cudaEventDestroy(tr_out[i]);
+    }
+    cudaEventDestroy(tr0);
+  }
   for (int i = 0; i < nch; ++i) {
     cudaEventDestroy(ev_in[i]);
     cudaEventDestroy(ev_done[i]);

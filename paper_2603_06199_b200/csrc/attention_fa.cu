@@ -20,6 +20,8 @@
 // plan-row fetch + range check + compaction, two items ahead per slot); w4..w7 softmax/epilogue
 // slot 0; w8..w11 softmax/epilogue slot 1.  PV(j) is issued in two K-halves, each released as
 // soon as that half of P is in TMEM.
+#include <cstdlib>
+
 #include "fp_kernels.h"
 
 namespace fpb {
@@ -48,6 +50,7 @@ struct FaParams {
   uint16_t* lists;  // global scratch: [grid][2 slots][2 bufs][M] compacted plan rows
   int num_items;
   int out_bf16;
+  int gs;     // KV groups per super-group of the work order (divides Hkv)
 };
 
 #ifdef FPB_TRACE
@@ -90,11 +93,20 @@ struct FaSmem {
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ void decode(const Dims& D, int item, int& z, int& h, int& qi) {
-  h = item % D.Hq;
-  const int t = item / D.Hq;
+// Work-item order: (z, KV super-group, query block heavy-first, head within the super-group).
+// A super-group is `gs` adjacent KV groups.  The Q heads of one KV group are adjacent within a
+// query block, so their K/V tiles are fetched once and re-read from L2; `gs` bounds the K/V
+// working set of the ~296 concurrent items to gs groups (chosen on the host so that it stays
+// well inside the 126 MB L2).  gs == Hkv is "all heads fastest" (best while everything fits).
+__device__ __forceinline__ void decode(const Dims& D, int gs, int item, int& z, int& h, int& qi) {
+  const int hs = gs * D.group;
+  const int hh = item % hs;
+  int t = item / hs;
   qi = D.M - 1 - (t % D.M);  // heavy (long rows) first
-  z = t / D.M;
+  t /= D.M;
+  const int nsg = D.Hkv / gs;
+  h = (t % nsg) * hs + hh;
+  z = t / nsg;
 }
 
 // Per-slot progress shared by the producer's and the MMA issuer's identical unit schedules.
@@ -176,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int nblk = 0;
         if (item >= 0) {
           int z, h, qi;
-          decode(D, item, z, h, qi);
+          decode(D, prm.gs, item, z, h, qi);
           if (dense) {
             nblk = qi + 1;
           } else {
@@ -250,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             continue;
           }
           int z, h, qi;
-          decode(D, S.item, z, h, qi);
+          decode(D, prm.gs, S.item, z, h, qi);
           {
             TR_T0();
             if (S.qc >= 1) mbar_wait(smem_u32(&s.q_empty[sl]), (S.qc - 1) & 1);
@@ -268,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // ---- one unit: V(j-1) then K(j), matching the MMA issue order PV(j-1), QK(j)
         int z, h, qi;
-        decode(D, S.item, z, h, qi);
+        decode(D, prm.gs, S.item, z, h, qi);
         const int zkv = z * D.Hkv + h / D.group;
         const uint16_t* lst = list_of(sl, p);
         if (S.j >= 1) push(&tm_v, (dense ? S.j - 1 : (int)lst[S.j - 1]) * kBlock, zkv);
@@ -389,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (item < 0) break;
       const uint16_t* lst = list_of(sl, p);
       int z, h, qi;
-      decode(D, item, z, h, qi);
+      decode(D, prm.gs, item, z, h, qi);
       const int rows = block_len(D, qi);
       float m_used = -INFINITY, l = 0.f;
       for (int n = 0; n < nblk; ++n, ++bc) {
@@ -585,8 +597,22 @@ cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __n
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int num_items = D.Z * D.Hq * D.M;
   const int grid = num_items < sms ? num_items : sms;
+  // K/V bytes of one KV group = 2 tensors x L x d x 2 B; keep gs groups' worth <= 64 MiB
+  // (measured: 32K prefers all 4 Qwen3 groups interleaved, 128K/256K one group at a time).
+  // FPB_FA_GS overrides (measurement switch).
+  static const int gs_env = [] {
+    const char* e = std::getenv("FPB_FA_GS");
+    return e ? std::atoi(e) : 0;
+  }();
+  int gs = gs_env;
+  if (gs <= 0) {
+    const double group_bytes = 2.0 * D.L * D.d * 2.0;
+    gs = (int)((64.0 * 1024 * 1024) / group_bytes);
+  }
+  gs = gs < 1 ? 1 : (gs > D.Hkv ? D.Hkv : gs);
+  while (D.Hkv % gs) --gs;
   FaParams prm{D, idx, counts, out, lse, visits, plan_error, sched, lists, num_items,
-               out_bf16 ? 1 : 0};
+               out_bf16 ? 1 : 0, gs};
   const size_t smem = sizeof(FaSmem) + 1024;
   e = cudaFuncSetAttribute(fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -123,19 +123,23 @@ constexpr size_t kSchedBytes = 1024;
 size_t ws_discover(const Dims& D, fpb_dtype t) {
   if (!tc_path(D))
     return align_up(pooled_bytes(D)) + 3 * align_up(map_elems(D) * 4) + align_up(map_elems(D));
-  size_t b = kSchedBytes + align_up(kbar_split_bytes(D));
+  size_t b = kSchedBytes + align_up(kbar_split_bytes(D)) + align_up(discover_scratch_bytes(D));
   if (t == FPB_F32) b += align_up(2 * q_elems(D) * 2);
   return b;
 }
 struct DiscWs {
   int* sched;
   __nv_bfloat16* kbar;
+  float* mscratch;         // long sequences only (discover_scratch_bytes)
   __nv_bfloat16* qplanes;  // fp32 inputs only
 };
 DiscWs disc_ws(const Dims& D, void* ws) {
   uint8_t* w = static_cast<uint8_t*>(ws);
+  const size_t o1 = kSchedBytes + align_up(kbar_split_bytes(D));
+  const size_t sb = discover_scratch_bytes(D);
   return {reinterpret_cast<int*>(w), reinterpret_cast<__nv_bfloat16*>(w + kSchedBytes),
-          reinterpret_cast<__nv_bfloat16*>(w + kSchedBytes + align_up(kbar_split_bytes(D)))};
+          sb ? reinterpret_cast<float*>(w + o1) : nullptr,
+          reinterpret_cast<__nv_bfloat16*>(w + o1 + align_up(sb))};
 }
 // attention: [sched][plan-row scratch] + fp32: Q hi/lo, K hi/lo, V bf16
 size_t ws_attention(const Dims& D, fpb_dtype t) {
@@ -253,7 +257,8 @@ int fpb_approx_block_scores(const fpb_problem* p, fpb_dtype dtype, const void* Q
   o.energy = energy;
   o.local_max = local_max;
   o.normalize = false;
-  FPB_CUDA(launch_discover(D, dtype == FPB_F32 ? 2 : 1, qp, w.kbar, o, w.sched, S(stream)));
+  FPB_CUDA(launch_discover(D, dtype == FPB_F32 ? 2 : 1, qp, w.kbar, o, w.sched, w.mscratch,
+                           S(stream)));
   return FPB_OK;
 }
 
@@ -308,7 +313,8 @@ int fpb_discover_select(const fpb_problem* p, fpb_dtype dtype, const void* Q, co
   o.mask = mask;
   o.idx = idx;
   o.counts = counts;
-  FPB_CUDA(launch_discover(D, dtype == FPB_F32 ? 2 : 1, qp, w.kbar, o, w.sched, S(stream)));
+  FPB_CUDA(launch_discover(D, dtype == FPB_F32 ? 2 : 1, qp, w.kbar, o, w.sched, w.mscratch,
+                           S(stream)));
   return FPB_OK;
 }
 

@@ -22,6 +22,8 @@
 //   w4..w7, w8..w11  two epilogue warpgroups, items alternating: TMEM -> (m, S) per pair, then
 //          row normalisation, threshold and compaction for the item while the MMA warp and the
 //          other warpgroup already work on the next ones.
+#include <cstdlib>
+
 #include "fp_kernels.h"
 
 namespace fpb {
@@ -42,6 +44,7 @@ struct DiscParams {
   DiscoverOut out;
   int* sched;      // zeroed work counter
   int num_items;
+  float* mscratch;  // per-CTA m/S rows in global memory when they do not fit in shared memory
 };
 
 template <int NQ>
@@ -55,9 +58,9 @@ struct DiscSmem {
   uint64_t it_full[kItemRing], it_empty[kItemRing];
   int items[kItemRing];
   uint32_t tmem_base;
-  float red[2][8];
-  int ired[2][8];
-  // followed by float m_s[M], S_s[M] per epilogue warpgroup (dynamic)
+  float red[2][3][4];
+  // followed by float m_s[M], S_s[M] per epilogue warpgroup, then int counts[ceil(M/128)][4]
+  // per epilogue warpgroup (dynamic)
 };
 
 __device__ __forceinline__ void decode_item(const Dims& D, int item, int& z, int& h, int& I) {
@@ -65,34 +68,6 @@ __device__ __forceinline__ void decode_item(const Dims& D, int item, int& z, int
   const int t = item / D.Hq;
   I = D.M - 1 - (t % D.M);  // heavy rows first
   z = t / D.M;
-}
-
-// Reductions over the 128 epilogue threads (named barrier kEpiBar).
-__device__ __forceinline__ float epi_max(float v, float* red, uint32_t bar) {
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  named_bar_sync(bar, kEpiThreads);
-  if (lane_id() == 0) red[warp_id() & 3] = v;
-  named_bar_sync(bar, kEpiThreads);
-  return fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
-}
-__device__ __forceinline__ float epi_sum(float v, float* red, uint32_t bar) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  named_bar_sync(bar, kEpiThreads);
-  if (lane_id() == 0) red[warp_id() & 3] = v;
-  named_bar_sync(bar, kEpiThreads);
-  return (red[0] + red[1]) + (red[2] + red[3]);
-}
-__device__ __forceinline__ int epi_prefix(bool pred, int* ired, int* total, uint32_t bar) {
-  const int w = warp_id() & 3, l = lane_id();
-  const unsigned bal = __ballot_sync(0xffffffffu, pred);
-  named_bar_sync(bar, kEpiThreads);
-  if (l == 0) ired[w] = __popc(bal);
-  named_bar_sync(bar, kEpiThreads);
-  int before = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) before += (i < w) ? ired[i] : 0;
-  *total = ired[0] + ired[1] + ired[2] + ired[3];
-  return before + __popc(bal & ((1u << l) - 1u));
 }
 
 template <int NQ>
@@ -221,15 +196,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ===================== epilogue: two warpgroups, items alternate between them
+    // Thread et owns key blocks J = c*128 + et (TMEM lane et of every chunk c) end to end, so the
+    // per-J state (m_s, S_s) never crosses threads and an item needs only three barrier rounds:
+    // row max of m, (sum, max) of the rescaled energies, and the compaction counts.
     const int wg = (warp - 4) >> 2;
     const uint32_t ebar = kEpiBar + wg;
-    float* red = s.red[wg];
-    int* ired = s.ired[wg];
-    float* m_s = reinterpret_cast<float*>(&s + 1) + (size_t)wg * 2 * D.M;
+    const int w4 = warp & 3;
+    float(*red)[4] = s.red[wg];       // [0]: row max, [1]/[2]: total / max of S'
+    const int nck = (D.M + kBlock - 1) / kBlock;
+    float* dyn = reinterpret_cast<float*>(&s + 1);
+    // m_s/S_s rows are thread-owned (J = c*128 + et): shared memory, or a per-CTA global
+    // scratch (coalesced, L1-resident) for sequences whose rows do not fit next to the rings
+    float* m_s = prm.mscratch ? prm.mscratch + ((size_t)blockIdx.x * 2 + wg) * 2 * D.M
+                              : dyn + (size_t)wg * 2 * D.M;
     float* S_s = m_s + D.M;
+    int* ired = reinterpret_cast<int*>(dyn + (prm.mscratch ? 0 : 4 * (size_t)D.M)) +
+                (size_t)wg * 4 * nck;  // [chunk][warp] active counts
     const int et = (threadIdx.x - 128) & 127;  // 0..127 within the warpgroup
-    const int jl = et;                         // TMEM lane == key block within a chunk
-    const uint32_t lane_addr = static_cast<uint32_t>(((warp - 4) & 3) * 32) << 16;
+    const uint32_t lane_addr = static_cast<uint32_t>(w4 * 32) << 16;
     const int N = D.M;
     int dc = 0;
     for (int t = wg;; t += 2) {
@@ -243,14 +227,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       decode_item(D, item, z, h, I);
       const int rows = block_len(D, I);
       const int nchunks = I / kBlock + 1;
+      float tmax = kNegSentinel;  // this thread's max of m over its J <= I
 
       // ---- per chunk: TMEM row J -> (local max m, energy S)  (discovery.hpp:96-110)
       for (int c = 0; c < nchunks; ++c, ++dc) {
         const int buf = wg * 2 + (dc & 1);
         mbar_wait(smem_u32(&s.d_full[buf]), (dc >> 1) & 1);
         tc_fence_after();
-        const int J = c * kBlock + jl;
-        const bool warp_live = c * kBlock + (int)((warp - 4) & 3) * 32 <= I;  // warp-uniform
+        const int J = c * kBlock + et;
+        const bool warp_live = c * kBlock + w4 * 32 <= I;  // warp-uniform
         float m = kNegSentinel, S = 0.f;
         if (warp_live) {
           uint32_t v[128];
@@ -260,39 +245,67 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(base + 64, *reinterpret_cast<uint32_t(*)[32]>(&v[64]));
           tmem_ld32(base + 96, *reinterpret_cast<uint32_t(*)[32]>(&v[96]));
           tmem_ld_wait();
-          // max commutes with the positive scale: max_r fl(a_r t) == fl(max_r(a_r) t)
-          float amax = -INFINITY;
+          // TMEM is in registers: release the accumulator to the MMA warp right away
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&s.d_empty[buf]));
+          // max commutes with the positive scale: max_r fl(a_r t) == fl(max_r(a_r) t).
+          // Four independent chains (max is exact, so the order is free).
+          float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
           if (rows == kBlock) {
 #pragma unroll
-            for (int r = 0; r < 128; ++r) amax = fmaxf(amax, __uint_as_float(v[r]));
+            for (int r = 0; r < 128; r += 4) {
+              a0 = fmaxf(a0, __uint_as_float(v[r]));
+              a1 = fmaxf(a1, __uint_as_float(v[r + 1]));
+              a2 = fmaxf(a2, __uint_as_float(v[r + 2]));
+              a3 = fmaxf(a3, __uint_as_float(v[r + 3]));
+            }
           } else {
 #pragma unroll
-            for (int r = 0; r < 128; ++r)
-              if (r < rows) amax = fmaxf(amax, __uint_as_float(v[r]));
+            for (int r = 0; r < 128; r += 4) {
+              a0 = fmaxf(a0, r < rows ? __uint_as_float(v[r]) : -INFINITY);
+              a1 = fmaxf(a1, r + 1 < rows ? __uint_as_float(v[r + 1]) : -INFINITY);
+              a2 = fmaxf(a2, r + 2 < rows ? __uint_as_float(v[r + 2]) : -INFINITY);
+              a3 = fmaxf(a3, r + 3 < rows ? __uint_as_float(v[r + 3]) : -INFINITY);
+            }
           }
-          m = __fmul_rn(amax, D.to_bits);
+          m = __fmul_rn(fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)), D.to_bits);
           const float nm = -m;
+          // S = sum_r exp2(x_r - m) over the tile's real rows (discovery.hpp:101-107) in four
+          // interleaved partial sums (the exp2 is ex2.approx, so the reference's sequential
+          // rounding is not reproduced bit-for-bit anyway; scores stay within 1e-6 relative)
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
           if (rows == kBlock) {
 #pragma unroll
-            for (int r = 0; r < 128; ++r)  // sequential r order (discovery.hpp:107)
-              S = __fadd_rn(S, ex2_approx(fmaf(__uint_as_float(v[r]), D.to_bits, nm)));
+            for (int r = 0; r < 128; r += 4) {
+              s0 += ex2_approx(fmaf(__uint_as_float(v[r]), D.to_bits, nm));
+              s1 += ex2_approx(fmaf(__uint_as_float(v[r + 1]), D.to_bits, nm));
+              s2 += ex2_approx(fmaf(__uint_as_float(v[r + 2]), D.to_bits, nm));
+              s3 += ex2_approx(fmaf(__uint_as_float(v[r + 3]), D.to_bits, nm));
+            }
           } else {
 #pragma unroll
-            for (int r = 0; r < 128; ++r)
-              if (r < rows) S = __fadd_rn(S, ex2_approx(fmaf(__uint_as_float(v[r]), D.to_bits, nm)));
+            for (int r = 0; r < 128; r += 4) {
+              s0 += r < rows ? ex2_approx(fmaf(__uint_as_float(v[r]), D.to_bits, nm)) : 0.f;
+              s1 += r + 1 < rows ? ex2_approx(fmaf(__uint_as_float(v[r + 1]), D.to_bits, nm)) : 0.f;
+              s2 += r + 2 < rows ? ex2_approx(fmaf(__uint_as_float(v[r + 2]), D.to_bits, nm)) : 0.f;
+              s3 += r + 3 < rows ? ex2_approx(fmaf(__uint_as_float(v[r + 3]), D.to_bits, nm)) : 0.f;
+            }
           }
+          S = (s0 + s1) + (s2 + s3);
+        } else {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&s.d_empty[buf]));
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&s.d_empty[buf]));
         if (J <= I) {
           m_s[J] = m;
           S_s[J] = S;
+          tmax = fmaxf(tmax, m);
         }
       }
-      named_bar_sync(ebar, kEpiThreads);
 
-      // ---- outputs: energy / local_max rows, normalisation (discovery.hpp:131-143)
+      // ---- outputs: energy / local_max rows (thread-owned J), then normalisation
       const size_t map_row = (((size_t)z * D.Hq + h) * D.M + I) * (size_t)N;
       if (prm.out.energy || prm.out.local_max) {
         for (int J = et; J < N; J += kEpiThreads) {
@@ -301,45 +314,69 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (prm.out.normalize) {
-        float rmax = kNegSentinel;
-        for (int J = et; J <= I; J += kEpiThreads) rmax = fmaxf(rmax, m_s[J]);
-        rmax = epi_max(rmax, red, ebar);
-        float total = 0.f;
+        // round 1: M_I = max_J m (discovery.hpp:131-134)
+        for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+        if (lane == 0) red[0][w4] = tmax;
+        named_bar_sync(ebar, kEpiThreads);
+        const float rmax = fmaxf(fmaxf(red[0][0], red[0][1]), fmaxf(red[0][2], red[0][3]));
+        // S'_J = S_J exp2(m_J - M_I); total = sum S'; max S' (for the threshold) in one round
+        float total = 0.f, pmax = 0.f;
         for (int J = et; J <= I; J += kEpiThreads) {
           const float r = __fmul_rn(S_s[J], ex2_approx(__fsub_rn(m_s[J], rmax)));
           S_s[J] = r;
           total += r;
+          pmax = fmaxf(pmax, r);
         }
-        total = epi_sum(total, red, ebar);
-        const float inv = __fdiv_rn(1.0f, __fadd_rn(total, D.eps));
-        float smax = 0.0f;  // selection.hpp:75
-        for (int J = et; J <= I; J += kEpiThreads) {
-          const float sc = __fmul_rn(S_s[J], inv);
-          S_s[J] = sc;
-          smax = fmaxf(smax, sc);
+        for (int o = 16; o > 0; o >>= 1) {
+          total += __shfl_xor_sync(0xffffffffu, total, o);
+          pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
         }
+        if (lane == 0) {
+          red[1][w4] = total;
+          red[2][w4] = pmax;
+        }
+        named_bar_sync(ebar, kEpiThreads);
+        total = (red[1][0] + red[1][1]) + (red[1][2] + red[1][3]);
+        pmax = fmaxf(fmaxf(red[2][0], red[2][1]), fmaxf(red[2][2], red[2][3]));
+        const float inv = __fdiv_rn(1.0f, __fadd_rn(total, D.eps));  // discovery.hpp:141-142
         if (prm.out.score)
           for (int J = et; J < N; J += kEpiThreads)
-            prm.out.score[map_row + J] = (J <= I) ? S_s[J] : 0.f;
+            prm.out.score[map_row + J] = (J <= I) ? __fmul_rn(S_s[J], inv) : 0.f;
 
         // ---- fused max-threshold + compaction (selection.hpp:63-92, 176-192)
-        if (prm.out.idx || prm.out.mask) {
-          smax = epi_max(smax, red, ebar);
+        if (prm.out.idx || prm.out.mask || prm.out.counts) {
+          // max_J fl(S'_J inv) == fl(max_J S'_J * inv): rounding is monotone for inv > 0;
+          // max_val starts at 0 (selection.hpp:75), scores are >= 0.
+          const float smax = __fmul_rn(pmax, inv);
           const float thresh = __fmul_rn(D.alpha, smax);
           const size_t plan_row = ((size_t)z * D.M + I) * (size_t)N;  // [z, I, :, :]
-          int base = 0;
-          for (int J0 = 0; J0 <= I; J0 += kEpiThreads) {
-            const int J = J0 + et;
-            bool act = false;
-            if (J <= I) act = (S_s[J] >= thresh) || J < D.sink_blocks || (I - J) < D.window_blocks;
-            int tot;
-            const int slot_j = base + epi_prefix(act, ired, &tot, ebar);
+          // round 3: per-(chunk, warp) active counts -> exclusive prefix in (J) order
+          auto active = [&](int J) {
+            return J <= I && ((__fmul_rn(S_s[J], inv) >= thresh) || J < D.sink_blocks ||
+                              (I - J) < D.window_blocks);
+          };
+          for (int c = 0; c < nchunks; ++c) {
+            const int J = c * kBlock + et;
+            const bool act = active(J);
+            const unsigned bal = __ballot_sync(0xffffffffu, act);
+            if (lane == 0) ired[c * 4 + w4] = __popc(bal);
             if (prm.out.mask && J < N) prm.out.mask[(plan_row + J) * D.Hq + h] = act ? 1 : 0;
-            if (prm.out.idx && act) prm.out.idx[(plan_row + slot_j) * D.Hq + h] = J;
-            base += tot;
+          }
+          named_bar_sync(ebar, kEpiThreads);
+          int base = 0;
+          for (int c = 0; c < nchunks; ++c) {
+            const int J = c * kBlock + et;
+            const bool act = active(J);
+            const unsigned bal = __ballot_sync(0xffffffffu, act);
+            int before = base;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) before += (w < w4) ? ired[c * 4 + w] : 0;
+            if (prm.out.idx && act)
+              prm.out.idx[(plan_row + before + __popc(bal & ((1u << lane) - 1u))) * D.Hq + h] = J;
+            base += (ired[c * 4 + 0] + ired[c * 4 + 1]) + (ired[c * 4 + 2] + ired[c * 4 + 3]);
           }
           if (prm.out.mask)
-            for (int J = (I / kEpiThreads + 1) * kEpiThreads + et; J < N; J += kEpiThreads)
+            for (int J = nchunks * kBlock + et; J < N; J += kEpiThreads)
               prm.out.mask[(plan_row + J) * D.Hq + h] = 0;
           if (prm.out.idx)
             for (int slot_j = base + et; slot_j < N; slot_j += kEpiThreads)
@@ -348,7 +385,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             prm.out.counts[((size_t)z * D.M + I) * D.Hq + h] = base;
         }
       }
-      named_bar_sync(ebar, kEpiThreads);  // m_s / S_s free for the next item
     }
   }
   tc_fence_before();
@@ -356,21 +392,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
+constexpr size_t kMaxSmem = 227 * 1024;
+
 template <int NQ>
-size_t disc_smem_bytes(int M) {
-  return sizeof(DiscSmem<NQ>) + 1024 + 4 * sizeof(float) * (size_t)M;
+size_t disc_smem_bytes(int M, bool rows_in_smem) {
+  return sizeof(DiscSmem<NQ>) + 1024 + (rows_in_smem ? 4 * sizeof(float) * (size_t)M : 0) +
+         2 * 4 * sizeof(int) * (size_t)((M + kBlock - 1) / kBlock);
+}
+
+int sm_count() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
 }
 
 template <int NQ>
 cudaError_t launch_nq(const Dims& D, const CUtensorMap& tm_q, const CUtensorMap& tm_kb,
                       const DiscParams& prm, cudaStream_t s) {
-  const size_t smem = disc_smem_bytes<NQ>(D.M);
+  const size_t smem = disc_smem_bytes<NQ>(D.M, prm.mscratch == nullptr);
   cudaError_t e = cudaFuncSetAttribute(discover_kernel<NQ>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count();
   const int grid = prm.num_items < sms ? prm.num_items : sms;
   discover_kernel<NQ><<<grid, kThreads, smem, s>>>(tm_q, tm_kb, prm);
   return cudaGetLastError();
@@ -378,16 +422,27 @@ cudaError_t launch_nq(const Dims& D, const CUtensorMap& tm_q, const CUtensorMap&
 
 }  // namespace
 
+size_t discover_scratch_bytes(const Dims& D) {
+  // FPB_DISC_FORCE_SCRATCH=1 takes the long-sequence path at any length (parity tests)
+  const char* force = std::getenv("FPB_DISC_FORCE_SCRATCH");
+  if (!(force && force[0] == '1') && disc_smem_bytes<1>(D.M, true) <= kMaxSmem &&
+      disc_smem_bytes<2>(D.M, true) <= kMaxSmem)
+    return 0;
+  return (size_t)sm_count() * 2 * 2 * sizeof(float) * D.M;
+}
+
 cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_planes,
                             const __nv_bfloat16* kbar_split, const DiscoverOut& out, int* sched,
-                            cudaStream_t s) {
+                            float* mscratch, cudaStream_t s) {
+  if (discover_scratch_bytes(D) == 0) mscratch = nullptr;
+  else if (!mscratch) return cudaErrorInvalidValue;
   CUtensorMap tm_q, tm_kb;
   if (!make_tmap_rows128(&tm_q, q_planes, D.L, (uint64_t)q_splits * D.Z * D.Hq) ||
       !make_tmap_rows128(&tm_kb, kbar_split, D.M, 2ull * D.Z * D.Hkv))
     return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(sched, 0, sizeof(int), s);
   if (e != cudaSuccess) return e;
-  DiscParams prm{D, out, sched, D.Z * D.Hq * D.M};
+  DiscParams prm{D, out, sched, D.Z * D.Hq * D.M, mscratch};
   return q_splits == 1 ? launch_nq<1>(D, tm_q, tm_kb, prm, s) : launch_nq<2>(D, tm_q, tm_kb, prm, s);
 }
 

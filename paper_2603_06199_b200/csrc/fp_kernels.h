@@ -39,7 +39,10 @@ struct DiscoverOut {
 };
 cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_planes,
                             const __nv_bfloat16* kbar_split, const DiscoverOut& out, int* sched,
-                            cudaStream_t s);
+                            float* mscratch, cudaStream_t s);
+// Global scratch launch_discover needs (0 while the per-key-block rows fit in shared memory,
+// i.e. up to ~270K tokens at B = 128).
+size_t discover_scratch_bytes(const Dims& D);
 
 // attention.cu / attention_fa.cu — block-sparse (idx/counts) or dense-causal (idx == nullptr).
 cudaError_t launch_attention(const Dims& D, int splits, const __nv_bfloat16* Q,

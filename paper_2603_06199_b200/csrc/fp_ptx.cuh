@@ -98,6 +98,14 @@ __device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const void* tmap,
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "l"(policy)
       : "memory");
 }
+// Prefetch a 3-D tile into L2 (no shared memory, no completion): hides HBM latency for a tile
+// that a later tma_load_3d will fetch.
+__device__ __forceinline__ void tma_prefetch_l2_3d(const void* tmap, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 // 3-D tiled TMA store shared -> global (bulk-group completion); OOB elements are clipped.
 __device__ __forceinline__ void tma_store_3d(const void* tmap, uint32_t src, int c0, int c1, int c2) {
   asm volatile(

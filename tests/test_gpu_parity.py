@@ -115,6 +115,49 @@ def test_fused_discover_select(fp, port, shape, alpha):
     assert np.array_equal(gi.transpose(0, 1, 3, 2)[ok_rows], idx.transpose(0, 1, 3, 2)[ok_rows])
 
 
+def test_fused_discover_select_global_rows(fp, port, monkeypatch):
+    """The long-sequence variant (per-key-block rows in a global scratch instead of shared memory,
+    taken automatically beyond ~270K tokens) forced at a size the oracle finishes quickly."""
+    monkeypatch.setenv("FPB_DISC_FORCE_SCRATCH", "1")
+    Z, Hq, Hkv, L = 1, 4, 2, 3000
+    q, k, v = composite_np(23, Z, Hq, Hkv, L)
+    q, k = bf16_round(q), bf16_round(k)
+    tau = float(port.scale(128))
+    _, _, sc = port.discover(q, k, 128, tau)
+    mask, _ = port.max_threshold_mask(sc, 128, 0.12, 256, 512)
+    idx, counts = port.compress_indices(mask)
+    plan, smap, gmask = fp.discover_select(_cuda(q), _cuda(k), fp.PipelineConfig(alpha=0.12),
+                                           want_score=True, want_mask=True)
+    bad, near, flipped = compare_masks(_np(gmask.active), mask, sc, 0.12)
+    assert bad == 0
+    ok_rows = ~rows_with_near(sc, 0.12)
+    assert np.array_equal(_np(plan.counts)[ok_rows], counts[ok_rows])
+    tri = np.broadcast_to(np.tril(np.ones(sc.shape[2:], bool)), sc.shape)
+    rs = np.abs(_np(smap.score) - sc) / np.maximum(sc, 1e-30)
+    assert rs[tri & (sc > 1e-6)].max() <= 1e-3
+
+
+def test_discover_select_300k_tokens(fp):
+    """Beyond the shared-memory row limit (M = 2344 key blocks): plan invariants of the reference
+    (selection.hpp:176-192): ascending indices, fill N, 1 <= C <= i+1, sinks + window kept."""
+    L, Hq, Hkv = 300_000, 2, 1
+    q, k, _ = fp.workload.composite(3, 1, Hq, Hkv, L, device="cuda")
+    plan = fp.discover_select(q, k, fp.PipelineConfig(alpha=0.12))[0]
+    M = (L + 127) // 128
+    idx = plan.indices[0].permute(2, 0, 1)  # h, i, slot
+    cnt = plan.counts[0].permute(1, 0)       # h, i
+    ar = torch.arange(M, device="cuda")
+    assert bool((cnt >= 1).all()) and bool((cnt <= ar + 1).all())
+    slots = torch.arange(M, device="cuda")[None, None, :]
+    live = slots < cnt[:, :, None]
+    assert bool((idx[~live] == M).all())
+    nxt = torch.where(live[:, :, 1:], idx[:, :, 1:], torch.full_like(idx[:, :, 1:], M + 1))
+    assert bool((nxt > idx[:, :, :-1]).all())
+    for i in (0, 5, M // 2, M - 1):  # the diagonal block (window) and block 0 (sink) are kept
+        row = idx[:, i, :]
+        assert bool((row == i).any(dim=1).all()) and bool((row[:, 0] == 0).all())
+
+
 # --------------------------------------------------------------------------- attention (K4/K5)
 def _attn_check(go, gl, ro, rl):
     mx, mean = err(go, ro)

@@ -414,52 +414,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         TR_ADD(0);  // softmax: waiting for S
         uint32_t v[128];
-        tmem_ld64(s_addr + 0, &v[0]);
-        tmem_ld64(s_addr + 64, &v[64]);
-        tmem_ld_wait();
-        if (!full) {
-#pragma unroll
-          for (int c = 0; c < 128; ++c)
-            if (c >= lim) v[c] = __float_as_uint(-INFINITY);
-        }
-        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 128; c += 8) {  // 4 independent 3-input max chains
-          mx0 = fmaxf(mx0, fmaxf(__uint_as_float(v[c + 0]), __uint_as_float(v[c + 1])));
-          mx1 = fmaxf(mx1, fmaxf(__uint_as_float(v[c + 2]), __uint_as_float(v[c + 3])));
-          mx2 = fmaxf(mx2, fmaxf(__uint_as_float(v[c + 4]), __uint_as_float(v[c + 5])));
-          mx3 = fmaxf(mx3, fmaxf(__uint_as_float(v[c + 6]), __uint_as_float(v[c + 7])));
-        }
-        const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
-        const float m_new = fmaxf(m_used, mx * D.to_bits);
-        TR_ADD(1);  // softmax: TMEM load + mask + row max
-        if (n == 0) {
-          m_used = m_new;
-        } else if (__any_sync(0xffffffffu, m_new > m_used + kRescaleThreshold)) {
-          // O must hold PV(n-1) before it is rescaled
-          mbar_wait(smem_u32(&s.o_done[sl]), (bc - 1) & 1);
-          tc_fence_after();
-          const float f = ex2_approx(m_used - m_new);
-#pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            uint32_t o[32];
-            tmem_ld32(o_addr + cc * 32, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * f);
-            tmem_st32(o_addr + cc * 32, o);
-          }
-          l *= f;
-          m_used = m_new;
-        }
-        TR_ADD(2);  // softmax: lazy O rescale (rare)
-        const float neg_m = -m_used, sc = D.to_bits;
+        const float sc = D.to_bits;
         float bs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        // causal diagonal / ragged tail: columns >= lim do not exist (attention.hpp:85-91)
+        auto mask_half = [&](int half) {
+          if (!full) {
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          // P packed in place: v[c/2] <- bf16x2(p_c, p_c+1); columns [64 half, 64 half + 64)
+            for (int c = half * 64; c < half * 64 + 64; ++c)
+              if (c >= lim) v[c] = __float_as_uint(-INFINITY);
+          }
+        };
+        auto max_half = [&](int half) {  // 4 independent 3-input max chains
+          float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+          for (int c = half * 64; c < half * 64 + 64; c += 8) {
+            mx0 = fmaxf(mx0, fmaxf(__uint_as_float(v[c + 0]), __uint_as_float(v[c + 1])));
+            mx1 = fmaxf(mx1, fmaxf(__uint_as_float(v[c + 2]), __uint_as_float(v[c + 3])));
+            mx2 = fmaxf(mx2, fmaxf(__uint_as_float(v[c + 4]), __uint_as_float(v[c + 5])));
+            mx3 = fmaxf(mx3, fmaxf(__uint_as_float(v[c + 6]), __uint_as_float(v[c + 7])));
+          }
+          return fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
+        };
+        // P = exp2(S * to_bits - m) for columns [64 half, 64 half + 64), packed in place:
+        // v[c/2] <- bf16x2(p_c, p_c+1); row sums in 8 independent accumulators
+        auto exp_half = [&](int half, float neg_m) {
           if (full) {
-            // MUFU-bound: every other pair of exponentials goes to the FMA pipe (exp2_poly2)
 #pragma unroll
             for (int c = half * 64; c < half * 64 + 64; c += 2) {
               float x0, x1, p0, p1;
@@ -484,6 +463,42 @@ __global__ void __launch_bounds__(kThreads, 1)
               v[c >> 1] = pack_bf16x2(p0, p1);
             }
           }
+        };
+        // lazy O rescale (exact: numerator and denominator share the stale max)
+        auto rescale = [&](float m_new) {
+          mbar_wait(smem_u32(&s.o_done[sl]), (bc - 1) & 1);  // O must hold PV(n-1)
+          tc_fence_after();
+          const float f = ex2_approx(m_used - m_new);
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            uint32_t o[32];
+            tmem_ld32(o_addr + cc * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * f);
+            tmem_st32(o_addr + cc * 32, o);
+          }
+          l *= f;
+          m_used = m_new;
+        };
+        {
+          tmem_ld64(s_addr + 0, &v[0]);
+          tmem_ld64(s_addr + 64, &v[64]);
+          tmem_ld_wait();
+          mask_half(0);
+          mask_half(1);
+          const float m_new = fmaxf(m_used, fmaxf(max_half(0), max_half(1)) * sc);
+          TR_ADD(1);  // softmax: TMEM load + mask + row max
+          if (n == 0)
+            m_used = m_new;
+          else if (__any_sync(0xffffffffu, m_new > m_used + kRescaleThreshold))
+            rescale(m_new);
+          TR_ADD(2);  // softmax: lazy O rescale (rare)
+          exp_half(0, -m_used);
+        }
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          if (half == 1) exp_half(1, -m_used);
           tmem_st32(s_addr + half * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[half * 32]));
           tmem_st_wait();
           tc_fence_before();

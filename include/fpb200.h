@@ -109,6 +109,26 @@ int fpb_block_sparse_attention(const fpb_problem* p, fpb_dtype dtype, const void
                                fpb_dtype out_dtype, void* out, float* lse,
                                unsigned long long* visits, int32_t* plan_error, void* workspace,
                                size_t workspace_bytes, void* stream);
+
+/* ---- Row-sharded execution (multi-GPU partition; no reference counterpart) ---------------- */
+/* Same as fpb_discover_select / fpb_block_sparse_attention restricted to the query blocks
+ * I = row_begin + row_step * k (0 <= row_begin < row_step).  Every (z, h, I) is independent
+ * (discovery.hpp:87-88, selection.hpp:71-72, attention.hpp:59-60), so row_step ranks with
+ * row_begin = rank split the work evenly whatever the per-head density; plan rows and output rows
+ * of blocks the shard does not own are left untouched.  Buffers keep the full-problem layout
+ * (every rank holds K/V and the pooled keys of the whole sequence).  d = block_size = 128 only. */
+int fpb_discover_select_rows(const fpb_problem* p, int32_t row_begin, int32_t row_step,
+                             fpb_dtype dtype, const void* Q, const void* K, float* energy,
+                             float* local_max, float* score, uint8_t* mask, int32_t* idx,
+                             int32_t* counts, void* workspace, size_t workspace_bytes,
+                             void* stream);
+int fpb_block_sparse_attention_rows(const fpb_problem* p, int32_t row_begin, int32_t row_step,
+                                    fpb_dtype dtype, const void* Q, const void* K, const void* V,
+                                    const int32_t* idx, const int32_t* counts,
+                                    fpb_dtype out_dtype, void* out, float* lse,
+                                    unsigned long long* visits, int32_t* plan_error,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+
 /* dense_attention (attention.hpp:135-174): the dense causal kernel, the speedup denominator. */
 int fpb_dense_attention(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
                         const void* V, fpb_dtype out_dtype, void* out, float* lse, void* workspace,

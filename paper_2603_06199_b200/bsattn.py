@@ -445,9 +445,12 @@ def density(plan: SparseBlockPlan, grid: BlockGrid) -> float:
 
 def discover_select(queries: torch.Tensor, keys: torch.Tensor, config: PipelineConfig,
                     want_score: bool = False, want_mask: bool = False,
-                    want_energy: bool = False):
+                    want_energy: bool = False, rows: tuple[int, int] | None = None):
     """Fused discover -> max_threshold_mask -> compress_indices (one pass over Q).
 
+    rows=(row_begin, row_step) restricts the work to query blocks row_begin + row_step * k
+    (fpb_discover_select_rows, the row-sharded multi-GPU partition); rows of other blocks in the
+    returned tensors are left unwritten.
     Returns (SparseBlockPlan, BlockScoreMap | None, ActiveMask | None)."""
     config.validate()
     _check_qk(queries, keys)
@@ -463,10 +466,16 @@ def discover_select(queries: torch.Tensor, keys: torch.Tensor, config: PipelineC
     lm = torch.empty_like(en) if want_energy else None
     mask = torch.empty((Z, M, M, Hq), dtype=torch.uint8, device=dev) if want_mask else None
     ws, nws = workspace(p, _dtype_code(queries), dev)
-    _raise(_abi.lib().fpb_discover_select(C.byref(p), _dtype_code(queries), _ptr(queries),
-                                          _ptr(keys), _ptr(en), _ptr(lm), _ptr(score), _ptr(mask),
-                                          _ptr(idx), _ptr(counts), _ptr(ws), nws,
-                                          _stream(queries)), "discover_select")
+    if rows is None:
+        _raise(_abi.lib().fpb_discover_select(C.byref(p), _dtype_code(queries), _ptr(queries),
+                                              _ptr(keys), _ptr(en), _ptr(lm), _ptr(score),
+                                              _ptr(mask), _ptr(idx), _ptr(counts), _ptr(ws), nws,
+                                              _stream(queries)), "discover_select")
+    else:
+        _raise(_abi.lib().fpb_discover_select_rows(
+            C.byref(p), int(rows[0]), int(rows[1]), _dtype_code(queries), _ptr(queries),
+            _ptr(keys), _ptr(en), _ptr(lm), _ptr(score), _ptr(mask), _ptr(idx), _ptr(counts),
+            _ptr(ws), nws, _stream(queries)), "discover_select_rows")
     smap = BlockScoreMap(en, lm, score) if want_score else None
     return SparseBlockPlan(idx, counts), smap, (ActiveMask(mask) if want_mask else None)
 
@@ -488,8 +497,12 @@ def _out_code(out_dtype, q):
 
 def block_sparse_attention(queries, keys, values, plan: SparseBlockPlan, grid: BlockGrid,
                            tau: float, stats: AttentionStats | None = None,
-                           out_dtype: torch.dtype | None = None) -> AttentionOutput:
-    """attention.hpp:38-132.  Raises PlanError for a block index outside [0, N)."""
+                           out_dtype: torch.dtype | None = None,
+                           rows: tuple[int, int] | None = None) -> AttentionOutput:
+    """attention.hpp:38-132.  Raises PlanError for a block index outside [0, N).
+
+    rows=(row_begin, row_step): only query blocks row_begin + row_step * k are computed
+    (fpb_block_sparse_attention_rows); output rows of other blocks are left unwritten."""
     _check_qkv(queries, keys, values)
     Z, Hq, L, d = queries.shape
     M = grid.num_query_blocks
@@ -504,11 +517,18 @@ def block_sparse_attention(queries, keys, values, plan: SparseBlockPlan, grid: B
     lse = torch.empty((Z, Hq, L), dtype=torch.float32, device=dev)
     aux = torch.zeros(2, dtype=torch.int64, device=dev)  # [visits, plan_error]
     ws, nws = workspace(p, _dtype_code(queries), dev)
-    _raise(_abi.lib().fpb_block_sparse_attention(
-        C.byref(p), _dtype_code(queries), _ptr(queries), _ptr(keys), _ptr(values), _ptr(idx),
-        _ptr(counts), oc, _ptr(out), _ptr(lse), C.c_void_p(aux.data_ptr()),
-        C.c_void_p(aux.data_ptr() + 8), _ptr(ws), nws, _stream(queries)),
-        "block_sparse_attention")
+    if rows is None:
+        _raise(_abi.lib().fpb_block_sparse_attention(
+            C.byref(p), _dtype_code(queries), _ptr(queries), _ptr(keys), _ptr(values), _ptr(idx),
+            _ptr(counts), oc, _ptr(out), _ptr(lse), C.c_void_p(aux.data_ptr()),
+            C.c_void_p(aux.data_ptr() + 8), _ptr(ws), nws, _stream(queries)),
+            "block_sparse_attention")
+    else:
+        _raise(_abi.lib().fpb_block_sparse_attention_rows(
+            C.byref(p), int(rows[0]), int(rows[1]), _dtype_code(queries), _ptr(queries),
+            _ptr(keys), _ptr(values), _ptr(idx), _ptr(counts), oc, _ptr(out), _ptr(lse),
+            C.c_void_p(aux.data_ptr()), C.c_void_p(aux.data_ptr() + 8), _ptr(ws), nws,
+            _stream(queries)), "block_sparse_attention_rows")
     visits, err = (int(x) for x in aux.tolist())
     if err:
         raise PlanError(f"plan row lists a block index outside [0, {M})")

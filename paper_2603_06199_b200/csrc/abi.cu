@@ -99,6 +99,21 @@ int resolve(const fpb_problem* p, Dims* D) {
   D->alpha = p->alpha;
   D->sink_blocks = (p->sink_tokens + D->B - 1) / D->B;      // core.hpp:103-105
   D->window_blocks = (p->window_tokens + D->B - 1) / D->B;  // core.hpp:106-108
+  D->rb = 0;
+  D->rs = 1;
+  D->Mr = D->M;
+  return FPB_OK;
+}
+
+// Restrict a resolved problem to the query blocks I = row_begin + row_step * k.
+int restrict_rows(Dims* D, int32_t row_begin, int32_t row_step) {
+  if (row_step < 1 || row_begin < 0 || row_begin >= row_step)
+    return fail(FPB_EVALIDATION, "row shard needs 0 <= row_begin < row_step");
+  if (row_step > 1 && !(D->d == kHeadDim && D->B == kBlock))
+    return fail(FPB_EVALIDATION, "row sharding needs d = block_size = 128");
+  D->rb = row_begin;
+  D->rs = row_step;
+  D->Mr = row_begin < D->M ? (D->M - row_begin + row_step - 1) / row_step : 0;
   return FPB_OK;
 }
 
@@ -272,12 +287,14 @@ int fpb_normalize_block_scores(const fpb_problem* p, const float* energy, const 
   return FPB_OK;
 }
 
-int fpb_discover_select(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
-                        float* energy, float* local_max, float* score, uint8_t* mask, int32_t* idx,
-                        int32_t* counts, void* workspace, size_t workspace_bytes, void* stream) {
+static int discover_select_rows(const fpb_problem* p, int32_t row_begin, int32_t row_step,
+                                fpb_dtype dtype, const void* Q, const void* K, float* energy,
+                                float* local_max, float* score, uint8_t* mask, int32_t* idx,
+                                int32_t* counts, void* workspace, size_t workspace_bytes,
+                                void* stream) {
   Dims D;
   int rc = resolve(p, &D);
-  if (rc || (rc = check_dtype(dtype))) return rc;
+  if (rc || (rc = check_dtype(dtype)) || (rc = restrict_rows(&D, row_begin, row_step))) return rc;
   if (!Q || !K) return fail(FPB_EUSAGE, "null pointer");
   if ((idx == nullptr) != (counts == nullptr))
     return fail(FPB_EUSAGE, "idx and counts must be given together");
@@ -303,6 +320,7 @@ int fpb_discover_select(const fpb_problem* p, fpb_dtype dtype, const void* Q, co
     }
     return FPB_OK;
   }
+  if (D.Mr == 0) return FPB_OK;  // this row shard owns no query block
   const DiscWs w = disc_ws(D, workspace);
   const __nv_bfloat16* qp;
   if ((rc = discover_prepare(D, dtype, Q, K, nullptr, w, S(stream), &qp))) return rc;
@@ -316,6 +334,22 @@ int fpb_discover_select(const fpb_problem* p, fpb_dtype dtype, const void* Q, co
   FPB_CUDA(launch_discover(D, dtype == FPB_F32 ? 2 : 1, qp, w.kbar, o, w.sched, w.mscratch,
                            S(stream)));
   return FPB_OK;
+}
+
+int fpb_discover_select(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
+                        float* energy, float* local_max, float* score, uint8_t* mask, int32_t* idx,
+                        int32_t* counts, void* workspace, size_t workspace_bytes, void* stream) {
+  return discover_select_rows(p, 0, 1, dtype, Q, K, energy, local_max, score, mask, idx, counts,
+                              workspace, workspace_bytes, stream);
+}
+
+int fpb_discover_select_rows(const fpb_problem* p, int32_t row_begin, int32_t row_step,
+                             fpb_dtype dtype, const void* Q, const void* K, float* energy,
+                             float* local_max, float* score, uint8_t* mask, int32_t* idx,
+                             int32_t* counts, void* workspace, size_t workspace_bytes,
+                             void* stream) {
+  return discover_select_rows(p, row_begin, row_step, dtype, Q, K, energy, local_max, score, mask,
+                              idx, counts, workspace, workspace_bytes, stream);
 }
 
 int fpb_discover(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
@@ -443,12 +477,16 @@ static int attention_common(const fpb_problem* p, fpb_dtype dtype, const void* Q
                             const void* V, const int32_t* idx, const int32_t* counts,
                             fpb_dtype out_dtype, void* out, float* lse,
                             unsigned long long* visits, int32_t* plan_error, void* workspace,
-                            size_t workspace_bytes, void* stream) {
+                            size_t workspace_bytes, void* stream, int32_t row_begin = 0,
+                            int32_t row_step = 1) {
   Dims D;
   int rc = resolve(p, &D);
-  if (rc || (rc = check_dtype(dtype)) || (rc = check_dtype(out_dtype))) return rc;
+  if (rc || (rc = check_dtype(dtype)) || (rc = check_dtype(out_dtype)) ||
+      (rc = restrict_rows(&D, row_begin, row_step)))
+    return rc;
   if (!Q || !K || !V || !out || !lse) return fail(FPB_EUSAGE, "null pointer");
   if ((rc = need_ws(workspace_bytes, ws_attention(D, dtype), workspace))) return rc;
+  if (D.Mr == 0) return FPB_OK;  // this row shard owns no query block
   if (!tc_path(D)) {
     FPB_CUDA(g_launch_attention(D, dtype == FPB_BF16, Q, K, V, idx, counts,
                                 out_dtype == FPB_BF16, out, lse, visits, plan_error,
@@ -492,6 +530,17 @@ int fpb_block_sparse_attention(const fpb_problem* p, fpb_dtype dtype, const void
   if (!idx || !counts) return fail(FPB_EUSAGE, "null plan");
   return attention_common(p, dtype, Q, K, V, idx, counts, out_dtype, out, lse, visits, plan_error,
                           workspace, workspace_bytes, stream);
+}
+
+int fpb_block_sparse_attention_rows(const fpb_problem* p, int32_t row_begin, int32_t row_step,
+                                    fpb_dtype dtype, const void* Q, const void* K, const void* V,
+                                    const int32_t* idx, const int32_t* counts,
+                                    fpb_dtype out_dtype, void* out, float* lse,
+                                    unsigned long long* visits, int32_t* plan_error,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  if (!idx || !counts) return fail(FPB_EUSAGE, "null plan");
+  return attention_common(p, dtype, Q, K, V, idx, counts, out_dtype, out, lse, visits, plan_error,
+                          workspace, workspace_bytes, stream, row_begin, row_step);
 }
 
 int fpb_dense_attention(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,

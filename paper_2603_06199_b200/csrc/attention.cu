@@ -74,8 +74,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int h = blockIdx.x % D.Hq;
   const int t = blockIdx.x / D.Hq;
-  const int qi = D.M - 1 - (t % D.M);
-  const int z = t / D.M;
+  const int qi = owned_row(D, t % D.Mr);
+  const int z = t / D.Mr;
   const int zkv = z * D.Hkv + h / D.group;
   const int rows = block_len(D, qi);
   const bool dense = prm.idx == nullptr;
@@ -346,7 +346,7 @@ cudaError_t launch_ns(const Dims& D, const CUtensorMap& tm_q, const CUtensorMap&
   cudaError_t e = cudaFuncSetAttribute(attention_kernel<NS>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const dim3 grid((unsigned)((size_t)D.Z * D.Hq * D.M));
+  const dim3 grid((unsigned)((size_t)D.Z * D.Hq * D.Mr));
   attention_kernel<NS><<<grid, kThreads, smem, s>>>(tm_q, tm_k, tm_v, prm);
   return cudaGetLastError();
 }

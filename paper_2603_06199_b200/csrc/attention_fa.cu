@@ -102,8 +102,8 @@ __device__ __forceinline__ void decode(const Dims& D, int gs, int item, int& z, 
   const int hs = gs * D.group;
   const int hh = item % hs;
   int t = item / hs;
-  qi = D.M - 1 - (t % D.M);  // heavy (long rows) first
-  t /= D.M;
+  qi = owned_row(D, t % D.Mr);  // heavy (long rows) first
+  t /= D.Mr;
   const int nsg = D.Hkv / gs;
   h = (t % nsg) * hs + hh;
   z = t / nsg;
@@ -610,7 +610,7 @@ cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __n
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int num_items = D.Z * D.Hq * D.M;
+  const int num_items = D.Z * D.Hq * D.Mr;
   const int grid = num_items < sms ? num_items : sms;
   // K/V bytes of one KV group = 2 tensors x L x d x 2 B; keep gs groups' worth <= 64 MiB
   // (measured: 32K prefers all 4 Qwen3 groups interleaved, 128K/256K one group at a time).

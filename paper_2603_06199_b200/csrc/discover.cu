@@ -66,8 +66,8 @@ struct DiscSmem {
 __device__ __forceinline__ void decode_item(const Dims& D, int item, int& z, int& h, int& I) {
   h = item % D.Hq;  // h fastest: co-running CTAs fill the head-last plan rows of one (z, I)
   const int t = item / D.Hq;
-  I = D.M - 1 - (t % D.M);  // heavy rows first
-  z = t / D.M;
+  I = owned_row(D, t % D.Mr);  // heavy rows first
+  z = t / D.Mr;
 }
 
 template <int NQ>
@@ -442,7 +442,7 @@ cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_
     return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(sched, 0, sizeof(int), s);
   if (e != cudaSuccess) return e;
-  DiscParams prm{D, out, sched, D.Z * D.Hq * D.M, mscratch};
+  DiscParams prm{D, out, sched, D.Z * D.Hq * D.Mr, mscratch};
   return q_splits == 1 ? launch_nq<1>(D, tm_q, tm_kb, prm, s) : launch_nq<2>(D, tm_q, tm_kb, prm, s);
 }
 

@@ -22,8 +22,18 @@ struct Dims {
   float eps, alpha;
   int sink_blocks, window_blocks;
   int B, d;                 // block size and head dim (128 / 128 on the tensor-core path)
+  // Row shard: only query blocks I = rb + rs * k (k < Mr) are processed (rb = 0, rs = 1,
+  // Mr = M for the whole problem).  Every (z, h, I) is independent (discovery.hpp:87-88,
+  // selection.hpp:71-72, attention.hpp:59-60), so rs ranks with rb = rank split any density
+  // profile evenly.
+  int rb, rs, Mr;
 };
 using GenDims = Dims;
+
+// t-th owned query block, heaviest (longest causal row) first.
+__host__ __device__ __forceinline__ int owned_row(const Dims& D, int t) {
+  return D.rb + D.rs * (D.Mr - 1 - t);
+}
 
 __host__ __device__ __forceinline__ int block_len(const Dims& D, int blk) {
   return blk + 1 == D.M ? D.last_len : D.B;

@@ -83,3 +83,50 @@ def gather_heads(out_local: torch.Tensor, lse_local: torch.Tensor, Hq: int, Hkv:
         out[:, q0:q0 + hl] = ob[r]
         lse[:, q0:q0 + hl] = lb[r]
     return out, lse
+
+
+# ----------------------------------------------------------------------------- row sharding
+# Strong scaling without the KV-group imbalance: rank r of G owns query blocks r, r + G, ...
+# of EVERY head (fpb_discover_select_rows / fpb_block_sparse_attention_rows with
+# row_begin = r, row_step = G).  Per-head densities differ a lot (the planted patterns, and real
+# heads), so KV-group shards finish at very different times (max/mean 1.8 at Qwen3 256K on 8
+# ranks, profiles/r1_lsweep.md); interleaved query blocks give every rank the same mix of heads
+# and row lengths.  Cost: every rank holds the whole K/V (2 x L x Hkv x d bf16: 512 MiB at 256K
+# Qwen3, trivial next to 180 GB of HBM) and pools all key blocks itself (~0.06 ms).
+
+def row_shard(world: int, rank: int) -> tuple[int, int]:
+    """(row_begin, row_step) of rank `rank` out of `world`."""
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    return rank, world
+
+
+def _row_blocks(x: torch.Tensor, block: int, world: int):
+    """Pad the L axis (dim 2) to a multiple of block * world and expose (.., M/world, world, B, ..)."""
+    Z, H, L = x.shape[:3]
+    M = -(-L // block)
+    Mw = -(-M // world) * world
+    if Mw * block != L:
+        pad = torch.zeros((Z, H, Mw * block) + tuple(x.shape[3:]), dtype=x.dtype, device=x.device)
+        pad[:, :, :L] = x
+        x = pad
+    return x.view((Z, H, Mw // world, world, block) + tuple(x.shape[3:])), L
+
+
+def gather_rows(out: torch.Tensor, lse: torch.Tensor, block: int, group=None):
+    """All-gather a row-sharded result.  Every rank holds full-size out (Z x Hq x L x d) and lse
+    (Z x Hq x L) with only its own query blocks written; returns the assembled tensors."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    res = []
+    for x in (out, lse):
+        xb, L = _row_blocks(x, block, world)
+        mine = xb[:, :, :, rank].contiguous()
+        allr = torch.empty((world * mine.shape[0],) + tuple(mine.shape[1:]), dtype=x.dtype,
+                           device=x.device)
+        dist.all_gather_into_tensor(allr, mine, group=group)
+        full = allr.view((world,) + tuple(mine.shape)).movedim(0, 3).contiguous()
+        full = full.view((x.shape[0], x.shape[1], -1) + tuple(x.shape[3:]))[:, :, :L]
+        res.append(full.contiguous())
+    return res[0], res[1]

@@ -1,0 +1,63 @@
+"""GPU: the row-sharded partition (fpb_discover_select_rows / fpb_block_sparse_attention_rows).
+
+Every (z, h, query block) is independent through discovery, selection and attention
+(discovery.hpp:87-88, selection.hpp:71-72, attention.hpp:59-60), so a rank that owns query blocks
+r, r + G, ... must produce exactly the plan rows and output rows of the unsharded call: the same
+kernels run the same per-item arithmetic, so the bar is bit-equality.
+"""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_row_shards_equal_whole(fp, world, dtype):
+    Z, Hq, Hkv, L = 2, 4, 2, 3000  # ragged last block, M = 24
+    q, k, v = fp.workload.composite(9, Z, Hq, Hkv, L, dtype=dtype, device="cuda")
+    cfg = fp.PipelineConfig(alpha=0.12)
+    grid = fp.make_block_grid(L, 128)
+    tau = 1 / math.sqrt(128)
+    M = grid.num_query_blocks
+    plan = fp.discover_select(q, k, cfg)[0]
+    whole = fp.block_sparse_attention(q, k, v, plan, grid, tau, out_dtype=torch.float32)
+    seen = torch.zeros(M, dtype=torch.bool)
+    for rank in range(world):
+        rows = (rank, world)
+        pr = fp.discover_select(q, k, cfg, rows=rows)[0]
+        own = list(range(rank, M, world))
+        seen[own] = True
+        assert torch.equal(pr.counts[:, own], plan.counts[:, own])
+        for I in own:  # live slots of each owned plan row (fill value N beyond the count)
+            assert torch.equal(pr.indices[:, I], plan.indices[:, I])
+        res = fp.block_sparse_attention(q, k, v, pr, grid, tau, out_dtype=torch.float32,
+                                        rows=rows)
+        for I in own:
+            sl = slice(I * 128, min(L, (I + 1) * 128))
+            assert torch.equal(res.out[:, :, sl], whole.out[:, :, sl])
+            assert torch.equal(res.lse[:, :, sl], whole.lse[:, :, sl])
+    assert bool(seen.all())
+
+
+def test_row_shard_beyond_blocks_is_noop(fp):
+    """A rank whose row_begin is past the last block owns nothing: both calls return without
+    touching their outputs."""
+    L = 256  # M = 2 blocks, rank 5 of 8 owns none
+    q, k, v = fp.workload.composite(1, 1, 2, 1, L, device="cuda")
+    cfg = fp.PipelineConfig()
+    plan = fp.discover_select(q, k, cfg)[0]
+    grid = fp.make_block_grid(L, 128)
+    pr = fp.discover_select(q, k, cfg, rows=(5, 8))[0]
+    assert pr.counts.shape == plan.counts.shape
+    fp.block_sparse_attention(q, k, v, plan, grid, 1 / math.sqrt(128), rows=(5, 8))
+
+
+def test_row_shard_validation(fp):
+    q, k, v = fp.workload.composite(1, 1, 2, 1, 512, device="cuda")
+    with pytest.raises(fp.ValidationError):
+        fp.discover_select(q, k, fp.PipelineConfig(), rows=(2, 2))
+    with pytest.raises(fp.ValidationError):
+        fp.discover_select(q, k, fp.PipelineConfig(), rows=(0, 0))

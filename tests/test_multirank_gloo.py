@@ -58,3 +58,38 @@ def test_two_rank_shard_and_gather():
     idx, counts = o.compress_indices(mask)
     out, lse, _ = o.block_sparse_attention(qn, kn, vn, idx, counts, 128, tau)
     assert np.array_equal(ret["out"], out) and np.array_equal(ret["lse"], lse)
+
+
+def _rows_worker(rank, world, port, out, lse, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_06199_b200.shard import gather_rows, row_shard
+    rb, rs = row_shard(world, rank)
+    L = out.shape[2]
+    own = torch.zeros(L, dtype=torch.bool)
+    for I in range(rb, -(-L // 128), rs):
+        own[I * 128:(I + 1) * 128] = True
+    # rows this rank does not own are garbage in its buffers (fpb_*_rows leaves them unwritten)
+    o = torch.where(own[None, None, :, None], out, torch.full_like(out, float("nan")))
+    l_ = torch.where(own[None, None, :], lse, torch.full_like(lse, -7.0))
+    go, gl = gather_rows(o, l_, 128)
+    if rank == 0:
+        ret["out"] = go.numpy()
+        ret["lse"] = gl.numpy()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_row_shard_gather_ragged_three_ranks():
+    """Row-sharded partition (query blocks r, r + G, ... per rank): the all-gather reassembles
+    the full output, including a ragged last block and M not divisible by the world size."""
+    g = torch.Generator().manual_seed(0)
+    Z, Hq, L, d = 2, 3, 1000, 128  # M = 8 blocks over 3 ranks
+    out = torch.randn((Z, Hq, L, d), generator=g)
+    lse = torch.randn((Z, Hq, L), generator=g)
+    world = 3
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_rows_worker, args=(world, _free_port(), out, lse, ret), nprocs=world, join=True)
+    assert np.array_equal(ret["out"], out.numpy()) and np.array_equal(ret["lse"], lse.numpy())

@@ -1,0 +1,137 @@
+#!/usr/bin/env python
+"""Sparse-prefill latency across sequence lengths at the Qwen3-30B-A3B layer shape (32 Q / 4 KV
+heads, d 128, bf16, alpha 0.12), one B200, plus one KV-group shard per rank at G = 2/4/8.
+
+Per length: pool / discover+select / sparse attention / dense K5 ms (CUDA events, median), density,
+effective TFLOP/s (dense-causal-equivalent), the attention kernel's algorithmic
+TFLOP/s and its fraction of the measured sustained bf16 peak, discovery GB/s against HBM.
+Shard rows: every rank's share (kv_group_shard) timed alone on this GPU; the G-GPU step is the max
+over ranks (no data-path collective; the O/LSE all-gather bytes per rank are listed, not timed:
+the pool gives one GPU per box).
+
+usage: python tools/lsweep.py [--Ls 4096,...] [--out profiles/r1_lsweep.jsonl]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2603_06199_b200 as fp  # noqa: E402
+from paper_2603_06199_b200 import shard, workload  # noqa: E402
+from tools.configs import timed  # noqa: E402
+
+D = 128
+HQ, HKV = 32, 4
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+    except OSError:
+        p = {}
+
+    def pick(*keys, default):
+        for k in keys:
+            if isinstance(p.get(k), (int, float)):
+                return float(p[k])
+        return default
+    return (pick("hbm_gbs", "hbm_gbps", default=6553.3),
+            pick("bf16_tflops_sustained", "bf16_dense_tflops_sustained", default=1399.3))
+
+
+def plan_flops(plan):
+    c = int(plan.counts.to(torch.int64).sum())
+    ndiag = plan.counts.numel()
+    return (c - ndiag) * 4.0 * D * 128 * 128 + ndiag * 4.0 * D * 128 * 129 / 2, c
+
+
+def stage(q, k, v, cfg, grid, tau, reps, rows=None):
+    hold = {}
+
+    def disc():
+        hold["p"] = fp.discover_select(q, k, cfg, rows=rows)[0]
+    t_disc = timed(disc, reps=reps, warm=1)
+    plan = hold["p"]
+    t_attn = timed(lambda: fp.block_sparse_attention(q, k, v, plan, grid, tau, rows=rows),
+                   reps=reps, warm=1)
+    if rows is not None:
+        return t_disc, t_attn, 0.0, 0
+    fl, visits = plan_flops(plan)
+    return t_disc, t_attn, fl, visits
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--Ls", default="4096,8192,16384,32768,65536,131072,262144")
+    ap.add_argument("--alpha", type=float, default=0.12)
+    ap.add_argument("--out", default="")
+    ap.add_argument("--no-dense", action="store_true")
+    args = ap.parse_args()
+    hbm, tc = peaks()
+    out = open(args.out, "a") if args.out else None
+    cfg = fp.PipelineConfig(alpha=args.alpha)
+    tau = cfg.resolved_scale(D)
+    for L in (int(x) for x in args.Ls.split(",")):
+        torch.cuda.empty_cache()
+        q, k, v = workload.composite(5, 1, HQ, HKV, L, device="cuda")
+        grid = fp.make_block_grid(L, 128)
+        M = grid.num_query_blocks
+        reps = 5 if L <= 65536 else 3
+        t_pool = timed(lambda: fp.pool_keys(k, grid), reps=reps, warm=1)
+        t_disc, t_attn, fl, visits = stage(q, k, v, cfg, grid, tau, reps)
+        dense_fl = 4.0 * D * HQ * L * (L + 1) / 2
+        disc_bytes = HQ * L * D * 2 + HKV * L * D * 2 + HQ * M * M * 4 + HQ * M * 4
+        rec = dict(L=L, alpha=args.alpha, G=1, density=visits / (HQ * M * (M + 1) / 2),
+                   visits=visits, pool_ms=t_pool, discover_select_ms=t_disc,
+                   attention_ms=t_attn, step_ms=t_disc + t_attn,
+                   eff_tflops=dense_fl / (t_disc + t_attn) / 1e9,
+                   attn_alg_tflops=fl / t_attn / 1e9, attn_frac=fl / t_attn / 1e9 / tc,
+                   disc_gbps=disc_bytes / t_disc / 1e6, disc_frac=disc_bytes / t_disc / 1e6 / hbm)
+        if not args.no_dense:
+            t_dense = timed(lambda: fp.dense_attention(q, k, v, tau), reps=2, warm=1)
+            rec.update(dense_ms=t_dense, speedup_vs_dense=t_dense / (t_disc + t_attn),
+                       dense_tflops=dense_fl / t_dense / 1e9)
+        line = json.dumps(rec)
+        print(line, flush=True)
+        if out:
+            out.write(line + "\n")
+            out.flush()
+        for G in (2, 4, 8):
+            for part in ("kv_group", "rows"):
+                per_rank = []
+                for rank in range(G):
+                    if part == "kv_group":
+                        s = shard.kv_group_shard(HQ, HKV, G, rank)
+                        ql, kl, vl = (x.contiguous() for x in shard.local_slices(q, k, v, s))
+                        td, ta, _, vis = stage(ql, kl, vl, cfg, grid, tau, reps)
+                    else:
+                        td, ta, _, vis = stage(q, k, v, cfg, grid, tau, reps,
+                                               rows=shard.row_shard(G, rank))
+                    per_rank.append((td + ta, td, ta, vis))
+                worst = max(per_rank)
+                gather = (G - 1) / G * HQ * L * (D * 2 + 4)  # bf16 O + fp32 LSE received per rank
+                rec = dict(L=L, alpha=args.alpha, G=G, partition=part,
+                           step_ms_max_over_ranks=worst[0],
+                           discover_select_ms=worst[1], attention_ms=worst[2],
+                           rank_step_ms=[round(x[0], 4) for x in per_rank],
+                           eff_tflops_job=dense_fl / worst[0] / 1e9,
+                           gather_bytes_per_rank=int(gather))
+                line = json.dumps(rec)
+                print(line, flush=True)
+                if out:
+                    out.write(line + "\n")
+                    out.flush()
+        del q, k, v
+
+
+if __name__ == "__main__":
+    main()

@@ -206,16 +206,23 @@ def run_gpu_arm(args, rank, world, dist):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    # the step as two CUDA graph launches over preallocated buffers (PrefillRunner): no host
+    # allocation, tensor-map encoding or synchronisation inside the timed region
+    runner = fp.PrefillRunner(q, k, v, cfg, out_dtype=torch.bfloat16)
+    if not args.no_graphs:
+        runner.capture()
+
     def step():
-        plan, _, _ = fp.discover_select(q, k, cfg)
+        runner.replay_discover()
         e_mid.record(stream)
-        res = fp.block_sparse_attention(q, k, v, plan, grid, tau, out_dtype=torch.bfloat16)
-        return plan, res
+        runner.replay_attend()
+        return runner.plan, runner
 
     e_mid = torch.cuda.Event(enable_timing=True)
     for _ in range(args.warmup):
         plan, res = step()
     torch.cuda.synchronize()
+    runner.check()  # PlanError surfaces here (plans come from discovery: never expected)
 
     t_step, t_disc, t_attn = [], [], []
     with ClockSampler(dev.index) as clocks:
@@ -318,7 +325,9 @@ def run_gpu_arm(args, rank, world, dist):
                    "global_batch_sequences": world, "seq_len": args.L,
                    "parallelism": f"shard (sequence, KV-head group) units over {world} GPU(s), "
                                   f"no data-path collective",
-                   "l2": "512 MiB buffer written between timed steps (L2 126 MB)"},
+                   "l2": "512 MiB buffer written between timed steps (L2 126 MB)",
+                   "launch": "CUDA graphs (PrefillRunner.capture)" if not args.no_graphs
+                             else "direct C-ABI launches"},
         "breakdown_ms": {"discover_select": ms_disc, "sparse_attention": ms_attn,
                          "dense_attention_k5": ms_dense},
         "speedup_vs_dense": ms_dense / ms, "speedup_attn_only": ms_dense / ms_attn,
@@ -359,6 +368,8 @@ def main():
     ap.add_argument("--n-vertical", type=int, default=8)
     ap.add_argument("--n-slash", type=int, default=4)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true",
+                    help="launch the two stages directly instead of replaying CUDA graphs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-heads", type=int, default=0)
     ap.add_argument("--ref-heads", type=int, default=0)

@@ -7,6 +7,7 @@ behind the C ABI in include/fpb200.h.  See DESIGN.md.
 from .bsattn import (  # noqa: F401
     ActiveMask, AttentionOutput, AttentionStats, BlockEnergies, BlockGrid, BlockScoreMap,
     ConfigError, CudaError, FormatError, IoError, PipelineConfig, PlanError, PooledKeys,
+    PrefillRunner,
     SelectionStats, SparseBlockPlan, ValidationError, approx_block_scores, block_sparse_attention,
     compress_indices, dense_attention, density, discover, discover_exact, discover_pool_both,
     discover_select, flops_dense_causal, topk_select, topp_select,

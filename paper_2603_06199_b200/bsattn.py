@@ -605,3 +605,108 @@ def flops_sparse(visits_off_diag: int, visits_diag: int, d: int = 128, B: int = 
     diagonal visit."""
     return 4.0 * d * (visits_off_diag * B * B + visits_diag * B * (B + 1) / 2.0)
 
+
+
+# ----------------------------------------------------------------------------- device-resident step
+class PrefillRunner:
+    """The device-resident FlashPrefill step with preallocated buffers, for serving loops and the
+    benchmark: fpb_discover_select then fpb_block_sparse_attention on the current stream, no host
+    allocation and no host synchronisation per step (the Python wrappers above sync once per call
+    to raise PlanError like the reference).  capture() records each stage into a CUDA graph, so a
+    step is two graph launches (the launch-bound inner loop without a tracing compiler).
+
+    rows=(row_begin, row_step) runs one rank's row shard (fpb_*_rows)."""
+
+    def __init__(self, queries, keys, values, config: PipelineConfig,
+                 out_dtype: torch.dtype = torch.bfloat16, rows: tuple[int, int] | None = None):
+        config.validate()
+        _check_qkv(queries, keys, values)
+        self.q, self.k, self.v = queries, keys, values
+        Z, Hq, L, d = queries.shape
+        self.grid = make_block_grid(L, config.block_size)
+        M = self.grid.num_query_blocks
+        dev = queries.device
+        self.p = problem(queries.shape, keys.shape[1], config=config)
+        self.dt = _dtype_code(queries)
+        self.out_dtype, self.oc = _out_code(out_dtype, queries)
+        self.rows = rows
+        self.idx = torch.empty((Z, M, M, Hq), dtype=torch.int32, device=dev)
+        self.counts = torch.empty((Z, M, Hq), dtype=torch.int32, device=dev)
+        self.out = torch.empty(queries.shape, dtype=self.out_dtype, device=dev)
+        self.lse = torch.empty((Z, Hq, L), dtype=torch.float32, device=dev)
+        self.aux = torch.zeros(2, dtype=torch.int64, device=dev)  # [visits, plan_error]
+        n = C.c_size_t(0)
+        _raise(_abi.lib().fpb_workspace_bytes(C.byref(self.p), self.dt, C.byref(n)), "workspace")
+        self.nws = n.value
+        self.ws = torch.empty(max(1, n.value), dtype=torch.uint8, device=dev)
+        self.graphs = None
+
+    @property
+    def plan(self) -> SparseBlockPlan:
+        return SparseBlockPlan(self.idx, self.counts)
+
+    def discover(self):
+        lib, s = _abi.lib(), _stream(self.q)
+        if self.rows is None:
+            rc = lib.fpb_discover_select(C.byref(self.p), self.dt, _ptr(self.q), _ptr(self.k),
+                                         None, None, None, None, _ptr(self.idx),
+                                         _ptr(self.counts), _ptr(self.ws), self.nws, s)
+        else:
+            rc = lib.fpb_discover_select_rows(C.byref(self.p), self.rows[0], self.rows[1], self.dt,
+                                              _ptr(self.q), _ptr(self.k), None, None, None, None,
+                                              _ptr(self.idx), _ptr(self.counts), _ptr(self.ws),
+                                              self.nws, s)
+        _raise(rc, "discover_select")
+
+    def attend(self):
+        lib, s = _abi.lib(), _stream(self.q)
+        vis, err = C.c_void_p(self.aux.data_ptr()), C.c_void_p(self.aux.data_ptr() + 8)
+        if self.rows is None:
+            rc = lib.fpb_block_sparse_attention(
+                C.byref(self.p), self.dt, _ptr(self.q), _ptr(self.k), _ptr(self.v), _ptr(self.idx),
+                _ptr(self.counts), self.oc, _ptr(self.out), _ptr(self.lse), vis, err,
+                _ptr(self.ws), self.nws, s)
+        else:
+            rc = lib.fpb_block_sparse_attention_rows(
+                C.byref(self.p), self.rows[0], self.rows[1], self.dt, _ptr(self.q), _ptr(self.k),
+                _ptr(self.v), _ptr(self.idx), _ptr(self.counts), self.oc, _ptr(self.out),
+                _ptr(self.lse), vis, err, _ptr(self.ws), self.nws, s)
+        _raise(rc, "block_sparse_attention")
+
+    def capture(self):
+        """Record discover and attend into two CUDA graphs (warm-up launch first)."""
+        side = torch.cuda.Stream(self.q.device)
+        side.wait_stream(torch.cuda.current_stream(self.q.device))
+        with torch.cuda.stream(side):
+            self.discover()
+            self.attend()
+        torch.cuda.current_stream(self.q.device).wait_stream(side)
+        torch.cuda.synchronize(self.q.device)
+        g_disc, g_attn = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        # relaxed: the launch helpers query device attributes while the stream is capturing
+        with torch.cuda.graph(g_disc, capture_error_mode="relaxed"):
+            self.discover()
+        with torch.cuda.graph(g_attn, capture_error_mode="relaxed"):
+            self.attend()
+        self.graphs = (g_disc, g_attn)
+        return self
+
+    def replay_discover(self):
+        if self.graphs:
+            self.graphs[0].replay()
+        else:
+            self.discover()
+
+    def replay_attend(self):
+        if self.graphs:
+            self.graphs[1].replay()
+        else:
+            self.attend()
+
+    def check(self) -> int:
+        """Synchronises; raises PlanError if any replay saw an out-of-range block index and
+        returns the accumulated block visits."""
+        visits, err = (int(x) for x in self.aux.tolist())
+        if err:
+            raise PlanError(f"plan row lists a block index outside [0, {self.grid.num_query_blocks})")
+        return visits

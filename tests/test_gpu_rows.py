@@ -61,3 +61,29 @@ def test_row_shard_validation(fp):
         fp.discover_select(q, k, fp.PipelineConfig(), rows=(2, 2))
     with pytest.raises(fp.ValidationError):
         fp.discover_select(q, k, fp.PipelineConfig(), rows=(0, 0))
+
+
+@pytest.mark.parametrize("rows", [None, (1, 2)])
+def test_prefill_runner_graph_replay(fp, rows):
+    """PrefillRunner (preallocated buffers, two CUDA graphs) reproduces the direct calls."""
+    Z, Hq, Hkv, L = 1, 4, 2, 2000
+    q, k, v = fp.workload.composite(4, Z, Hq, Hkv, L, device="cuda")
+    cfg = fp.PipelineConfig(alpha=0.1)
+    grid = fp.make_block_grid(L, 128)
+    plan = fp.discover_select(q, k, cfg)[0]
+    ref = fp.block_sparse_attention(q, k, v, plan, grid, cfg.resolved_scale(128),
+                                    out_dtype=torch.bfloat16)
+    r = fp.PrefillRunner(q, k, v, cfg, out_dtype=torch.bfloat16, rows=rows).capture()
+    for _ in range(3):
+        r.replay_discover()
+        r.replay_attend()
+    visits = r.check()
+    M = grid.num_query_blocks
+    own = list(range(M)) if rows is None else list(range(rows[0], M, rows[1]))
+    assert torch.equal(r.counts[:, own], plan.counts[:, own])
+    for I in own:
+        sl = slice(I * 128, min(L, (I + 1) * 128))
+        assert torch.equal(r.out[:, :, sl], ref.out[:, :, sl])
+        assert torch.equal(r.lse[:, :, sl], ref.lse[:, :, sl])
+    # 1 warm-up launch + 3 replays, visits accumulate per launch
+    assert visits == 4 * int(plan.counts[:, own].to(torch.int64).sum())

@@ -55,14 +55,12 @@ def plan_flops(plan):
 
 
 def stage(q, k, v, cfg, grid, tau, reps, rows=None):
-    hold = {}
-
-    def disc():
-        hold["p"] = fp.discover_select(q, k, cfg, rows=rows)[0]
-    t_disc = timed(disc, reps=reps, warm=1)
-    plan = hold["p"]
-    t_attn = timed(lambda: fp.block_sparse_attention(q, k, v, plan, grid, tau, rows=rows),
-                   reps=reps, warm=1)
+    """Device time of the two stages, each replayed from a CUDA graph (PrefillRunner)."""
+    r = fp.PrefillRunner(q, k, v, cfg, rows=rows).capture()
+    t_disc = timed(r.replay_discover, reps=reps, warm=1)
+    t_attn = timed(r.replay_attend, reps=reps, warm=1)
+    r.check()
+    plan = r.plan
     if rows is not None:
         return t_disc, t_attn, 0.0, 0
     fl, visits = plan_flops(plan)

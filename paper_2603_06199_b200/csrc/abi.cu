@@ -8,6 +8,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -561,11 +562,13 @@ struct Arena {
   size_t cap = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t s_in = nullptr, s_out = nullptr;  // copy streams of the pipelined prefill
+  cudaStream_t s_c2 = nullptr;                     // second compute stream of the prefill
   ~Arena() {
     if (ptr) cudaFree(ptr);
     if (stream) cudaStreamDestroy(stream);
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
+    if (s_c2) cudaStreamDestroy(s_c2);
   }
 };
 thread_local Arena g_arena;
@@ -908,13 +911,18 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
   const size_t wsd = ws_discover(Ds, dtype), wsa = ws_attention(Ds, dtype);
   const size_t wsb = wsd > wsa ? wsd : wsa;
   const size_t need = align_up(qb) + 2 * align_up(kb) + align_up(ob) + align_up(lb) +
-                      nch * (align_up(sib) + align_up(scb)) + align_up(8 * nch) + align_up(wsb);
+                      nch * (align_up(sib) + align_up(scb)) + align_up(8 * nch) +
+                      2 * align_up(wsb);
   uint8_t* base;
   cudaStream_t st;
   if ((rc = arena_get(need, &base, &st))) return rc;
   if (!g_arena.s_in) FPB_CUDA(cudaStreamCreateWithFlags(&g_arena.s_in, cudaStreamNonBlocking));
   if (!g_arena.s_out) FPB_CUDA(cudaStreamCreateWithFlags(&g_arena.s_out, cudaStreamNonBlocking));
+  if (!g_arena.s_c2) FPB_CUDA(cudaStreamCreateWithFlags(&g_arena.s_c2, cudaStreamNonBlocking));
   cudaStream_t s_in = g_arena.s_in, s_out = g_arena.s_out;
+  // chunks alternate between two compute streams with their own workspaces, so the next chunk's
+  // kernels fill the SMs that the current chunk's longest rows leave idle
+  cudaStream_t sc[2] = {st, g_arena.s_c2};
   Carve c{base};
   uint8_t* dq = c.take<uint8_t>(qb);
   uint8_t* dk = c.take<uint8_t>(kb);
@@ -922,7 +930,7 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
   uint8_t* dout = c.take<uint8_t>(ob);
   float* dl = c.take<float>(lb);
   unsigned long long* dvis = c.take<unsigned long long>(8 * nch);
-  void* ws = c.take<void>(wsb);
+  void* wsc[2] = {c.take<void>(wsb), c.take<void>(wsb)};
   std::vector<int32_t*> di(nch), dc(nch);
   for (int i = 0; i < nch; ++i) {
     di[i] = c.take<int32_t>(sib);
@@ -934,6 +942,13 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
     FPB_CUDA(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming));
   }
   FPB_CUDA(cudaMemsetAsync(dvis, 0, 8 * nch, st));
+  {  // the second compute stream starts after the memset (and any earlier use of the arena)
+    cudaEvent_t e0;
+    FPB_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    FPB_CUDA(cudaEventRecord(e0, st));
+    FPB_CUDA(cudaStreamWaitEvent(sc[1], e0, 0));
+    cudaEventDestroy(e0);
+  }
   // FPB_E2E_TRACE=1: per-chunk timeline (H2D done / kernels done / D2H done) on stderr
   static const bool trace = getenv("FPB_E2E_TRACE") != nullptr;
   std::vector<cudaEvent_t> tr_in, tr_k, tr_out;
@@ -965,22 +980,24 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
     FPB_CUDA(cudaEventRecord(ev_in[i], s_in));
     if ((rc = tr_mark(tr_in, s_in))) return rc;
   }
-  for (int i = 0; i < nch; ++i) {  // kernels of each chunk on the compute stream
+  for (int i = 0; i < nch; ++i) {  // kernels of each chunk on alternating compute streams
     const int z = i / chunks_per_z, q0 = (i % chunks_per_z) * cq, kv = q0 / group;
-    FPB_CUDA(cudaStreamWaitEvent(st, ev_in[i], 0));
+    cudaStream_t cs = sc[i & 1];
+    void* ws = wsc[i & 1];
+    FPB_CUDA(cudaStreamWaitEvent(cs, ev_in[i], 0));
     const uint8_t* q = dq + ((size_t)z * D.Hq + q0) * Ld * es;
     const uint8_t* k = dk + ((size_t)z * D.Hkv + kv) * Ld * es;
     const uint8_t* v = dv + ((size_t)z * D.Hkv + kv) * Ld * es;
     uint8_t* o = dout + ((size_t)z * D.Hq + q0) * Ld * eo;
     float* l = dl + ((size_t)z * D.Hq + q0) * D.L;
     if ((rc = fpb_discover_select(&sub, dtype, q, k, nullptr, nullptr, nullptr, nullptr, di[i],
-                                  dc[i], ws, wsb, st)))
+                                  dc[i], ws, wsb, cs)))
       return rc;
     if ((rc = fpb_block_sparse_attention(&sub, dtype, q, k, v, di[i], dc[i], out_dtype, o, l,
-                                         dvis + i, nullptr, ws, wsb, st)))
+                                         dvis + i, nullptr, ws, wsb, cs)))
       return rc;
-    FPB_CUDA(cudaEventRecord(ev_done[i], st));
-    if ((rc = tr_mark(tr_k, st))) return rc;
+    FPB_CUDA(cudaEventRecord(ev_done[i], cs));
+    if ((rc = tr_mark(tr_k, cs))) return rc;
   }
   uint8_t* ho = static_cast<uint8_t*>(out);
   for (int i = 0; i < nch; ++i) {  // D2H of each finished chunk
@@ -1004,6 +1021,7 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
   }
   std::vector<unsigned long long> vis(nch, 0);
   FPB_CUDA(cudaStreamSynchronize(st));
+  FPB_CUDA(cudaStreamSynchronize(sc[1]));
   FPB_CUDA(cudaMemcpyAsync(vis.data(), dvis, 8 * nch, cudaMemcpyDeviceToHost, s_out));
   FPB_CUDA(cudaStreamSynchronize(s_out));
   if (trace) {

@@ -9,8 +9,9 @@
 namespace fpb {
 
 // pool.cu
+// Pools key blocks [j0, j0 + nj) (all blocks by default).
 cudaError_t launch_pool_keys(const Dims& D, bool bf16_in, const void* K, float* pooled,
-                             __nv_bfloat16* kbar_split, cudaStream_t s);
+                             __nv_bfloat16* kbar_split, cudaStream_t s, int j0 = 0, int nj = -1);
 cudaError_t launch_split_pooled(const Dims& D, const float* pooled, __nv_bfloat16* kbar_split,
                                 cudaStream_t s);
 cudaError_t launch_f32_to_bf16(const float* src, __nv_bfloat16* hi, __nv_bfloat16* lo, size_t n,

@@ -15,9 +15,9 @@ template <bool kBf16>
 __global__ void __launch_bounds__(64) pool_keys_kernel(const void* __restrict__ K,
                                                        float* __restrict__ pooled,
                                                        __nv_bfloat16* __restrict__ split, int ZH,
-                                                       int L, int M, int last_len) {
-  // one CTA of 64 threads per (zh, key block j); thread t owns channels 2t, 2t+1
-  const int zh = blockIdx.x / M, j = blockIdx.x % M;
+                                                       int L, int M, int last_len, int j0, int nj) {
+  // one CTA of 64 threads per (zh, key block j in [j0, j0 + nj)); thread t owns channels 2t, 2t+1
+  const int zh = blockIdx.x / nj, j = j0 + blockIdx.x % nj;
   const int c0 = threadIdx.x * 2;
   const int len = (j + 1 == M) ? last_len : kBlock;
   const size_t row0 = (size_t)zh * L + (size_t)j * kBlock;
@@ -79,13 +79,17 @@ __global__ void __launch_bounds__(64) pool_keys_kernel(const void* __restrict__ 
 }
 
 cudaError_t launch_pool_keys(const Dims& D, bool bf16_in, const void* K, float* pooled,
-                             __nv_bfloat16* kbar_split, cudaStream_t s) {
+                             __nv_bfloat16* kbar_split, cudaStream_t s, int j0, int nj) {
   const int ZH = D.Z * D.Hkv;
-  const dim3 grid(ZH * D.M);
+  if (nj < 0) nj = D.M - j0;
+  if (nj <= 0) return cudaSuccess;
+  const dim3 grid(ZH * nj);
   if (bf16_in)
-    pool_keys_kernel<true><<<grid, 64, 0, s>>>(K, pooled, kbar_split, ZH, D.L, D.M, D.last_len);
+    pool_keys_kernel<true><<<grid, 64, 0, s>>>(K, pooled, kbar_split, ZH, D.L, D.M, D.last_len,
+                                               j0, nj);
   else
-    pool_keys_kernel<false><<<grid, 64, 0, s>>>(K, pooled, kbar_split, ZH, D.L, D.M, D.last_len);
+    pool_keys_kernel<false><<<grid, 64, 0, s>>>(K, pooled, kbar_split, ZH, D.L, D.M, D.last_len,
+                                                j0, nj);
   return cudaGetLastError();
 }
 

@@ -284,6 +284,32 @@ def test_prefill_host_e2e(fp, port):
     _attn_check(out.numpy(), lse.numpy(), ro, rl)
 
 
+@pytest.mark.parametrize("chunks", ["1", "3", "16"])
+def test_prefill_host_rows_equal_device(fp, monkeypatch, chunks):
+    """The row-chunked host pipeline (H2D of each chunk's token rows of every head, pooling,
+    discovery and attention of those rows, D2H) reproduces the device-resident calls bit for bit:
+    plan, output and LSE, including a ragged last block and Z = 2."""
+    monkeypatch.setenv("FPB_E2E_CHUNKS", chunks)
+    Z, Hq, Hkv, L = 2, 4, 2, 3000
+    q, k, v = fp.workload.composite(31, Z, Hq, Hkv, L)
+    cfg = fp.PipelineConfig(alpha=0.1)
+    grid = fp.make_block_grid(L, 128)
+    qd, kd, vd = (x.cuda() for x in (q, k, v))
+    plan = fp.discover_select(qd, kd, cfg)[0]
+    res = fp.block_sparse_attention(qd, kd, vd, plan, grid, cfg.resolved_scale(128),
+                                    out_dtype=torch.bfloat16)
+    qh, kh, vh = (x.pin_memory() for x in (q, k, v))
+    out = torch.empty(qh.shape, dtype=torch.bfloat16).pin_memory()
+    lse = torch.empty(qh.shape[:3], dtype=torch.float32).pin_memory()
+    M = grid.num_query_blocks
+    idx = torch.empty((Z, M, M, Hq), dtype=torch.int32)
+    counts = torch.empty((Z, M, Hq), dtype=torch.int32)
+    vis = fp.prefill_host(qh, kh, vh, cfg, out, lse, idx, counts)
+    assert torch.equal(counts, plan.counts.cpu()) and torch.equal(idx, plan.indices.cpu())
+    assert vis == int(counts.to(torch.int64).sum())
+    assert torch.equal(out, res.out.cpu()) and torch.equal(lse, res.lse.cpu())
+
+
 # --------------------------------------------------------------------------- committed goldens
 def _golden_cases():
     import glob

@@ -15,3 +15,4 @@ from .bsattn import (  # noqa: F401
     normalize_block_scores, pool_keys, prefill, prefill_host, visit_count,
 )
 from . import workload  # noqa: F401,E402  (synthetic inputs for bench / tests)
+from . import shard  # noqa: F401,E402  (multi-GPU partitions and gathers)

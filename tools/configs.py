@@ -50,17 +50,16 @@ def dense_flops(Z, H, L):
 
 
 def stage_times(q, k, v, cfg, out_dtype=torch.bfloat16):
+    """Device time of each stage, replayed from CUDA graphs (PrefillRunner): no host work in
+    the timed region.  discover+select includes its key pooling."""
     L = q.shape[2]
     grid = fp.make_block_grid(L, 128)
-    tau = cfg.resolved_scale(D)
     t_pool = timed(lambda: fp.pool_keys(k, grid))
-    holder = {}
-
-    def disc():
-        holder["plan"] = fp.discover_select(q, k, cfg)[0]
-    t_disc = timed(disc)
-    plan = holder["plan"]
-    t_attn = timed(lambda: fp.block_sparse_attention(q, k, v, plan, grid, tau, out_dtype=out_dtype))
+    r = fp.PrefillRunner(q, k, v, cfg, out_dtype=out_dtype).capture()
+    t_disc = timed(r.replay_discover)
+    t_attn = timed(r.replay_attend)
+    r.check()
+    plan = fp.SparseBlockPlan(r.idx.clone(), r.counts.clone())
     visits = int(plan.counts.to(torch.int64).sum())
     M = grid.num_query_blocks
     dens = visits / (q.shape[0] * q.shape[1] * M * (M + 1) / 2)
@@ -103,7 +102,7 @@ def c3(emit):
     q, k, v = workload.llama31_8b(L, seed=7, device="cuda")
     st, _ = stage_times(q, k, v, fp.PipelineConfig(alpha=0.18))
     t_dense = timed(lambda: fp.dense_attention(q, k, v, 1 / math.sqrt(D)), reps=2, warm=1)
-    emit(dict(config="C3 Llama-3.1-8B 64K bf16 alpha=0.18, 1 GPU", **st, dense_ms=t_dense,
+    emit(dict(config="C3 Llama-3.1-8B 64K bf16 alpha=0.18, 1 GPU", alpha=0.18, **st, dense_ms=t_dense,
               speedup_vs_dense=t_dense / st["step_ms"],
               eff_tflops=dense_flops(1, 32, L) / st["step_ms"] / 1e9))
     for G in (2, 4, 8):
@@ -111,7 +110,7 @@ def c3(emit):
         ql, kl, vl = shard.local_slices(q, k, v, s)
         st2, _ = stage_times(ql, kl, vl, fp.PipelineConfig(alpha=0.18))
         emit(dict(config=f"C3 Llama 64K: one rank's KV-group shard at G={G} "
-                         f"({s.hq} Q / {s.hkv} KV heads), timed alone on 1 GPU", **st2,
+                         f"({s.hq} Q / {s.hkv} KV heads), timed alone on 1 GPU", alpha=0.18, **st2,
                   eff_tflops_per_gpu=dense_flops(1, s.hq, L) / st2["step_ms"] / 1e9))
 
 
@@ -147,11 +146,47 @@ def c5(emit):
               **st2, eff_tflops_per_gpu=dense_flops(1, s.hq, L) / st2["step_ms"] / 1e9))
 
 
+def to_markdown(path):
+    """Render a configs .jsonl as the markdown table committed under profiles/."""
+    rows = [json.loads(x) for x in open(path)]
+    out = ["# BASELINE configs on one B200 (tools/configs.py; CUDA events, median of 5; stage "
+           "times are CUDA-graph replays; bf16 unless noted)", "",
+           "| config | alpha | density | visits | pool ms | discover+select ms | attention ms | "
+           "step ms | dense K5 ms | speedup vs dense | err max / mean vs dense |",
+           "|---|---|---|---|---|---|---|---|---|---|---|"]
+    for r in rows:
+        err = (f"{r['err_max_abs']:.3g} / {r['err_mean_abs']:.3g}" if "err_max_abs" in r else "-")
+        out.append(
+            f"| {r['config']} | {r.get('alpha', 0.12)} | {r['density']:.3f} | {r['visits']} | "
+            f"{r['pool_ms']:.3f} | {r['discover_select_ms']:.3f} | {r['attention_ms']:.3f} | "
+            f"{r['step_ms']:.3f} | {r['dense_ms']:.2f} | {r['speedup_vs_dense']:.2f} | {err} |"
+            if "dense_ms" in r else
+            f"| {r['config']} | {r.get('alpha', 0.12)} | {r['density']:.3f} | {r['visits']} | "
+            f"{r['pool_ms']:.3f} | {r['discover_select_ms']:.3f} | {r['attention_ms']:.3f} | "
+            f"{r['step_ms']:.3f} | - | - | {err} |")
+    c1 = [r for r in rows if r["config"].startswith("C1")]
+    if c1:
+        r = c1[0]
+        out += ["", f"C1 (fp32, 4K, 1 head): GPU step {r['step_ms']:.3f} ms vs the reference CPU "
+                    f"pipeline {r['cpu_reference_ms']:.1f} ms (1 thread, oracle/{r['cpu_kind']}) = "
+                    f"{r['speedup_vs_cpu']:.0f}x; same plan visits ({r['visits']} = "
+                    f"{r['cpu_visits']}); out max-abs {r['out_max_abs']:.2e}, mean-abs "
+                    f"{r['out_mean_abs']:.2e}, lse max-abs {r['lse_max_abs']:.2e}."]
+    out += ["Shard rows time ONE rank's KV-group shard alone on one GPU (the box has one GPU); "
+            "they are not multi-GPU measurements (profiles/r1_lsweep.md has every rank's share "
+            "and the row-sharded partition)."]
+    return "\n".join(out) + "\n"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="C1,C2,C3,C4,C5")
     ap.add_argument("--out", default="")
+    ap.add_argument("--markdown", default="", help="render this .jsonl and exit")
     args = ap.parse_args()
+    if args.markdown:
+        print(to_markdown(args.markdown), end="")
+        return
     f = open(args.out, "a") if args.out else None
 
     def emit(d):

@@ -158,6 +158,37 @@ def test_discover_select_300k_tokens(fp):
         assert bool((row == i).any(dim=1).all()) and bool((row[:, 0] == 0).all())
 
 
+@pytest.mark.parametrize("cfgv", [
+    dict(sink_tokens=0, window_tokens=1, alpha=0.12),        # no structural retention
+    dict(sink_tokens=1000, window_tokens=129, alpha=0.2),    # ceil-derived 8 sink / 2 window blocks
+    dict(sink_tokens=256, window_tokens=2000, alpha=0.05),   # wide window
+    dict(sink_tokens=256, window_tokens=512, alpha=0.12, scale=0.05),  # explicit tau
+    dict(sink_tokens=256, window_tokens=512, alpha=0.12, epsilon=1e-3),
+])
+@pytest.mark.parametrize("shape", [(1, 3, 1, 1537), (2, 6, 3, 777), (1, 2, 2, 100)])
+def test_config_variants_pipeline(fp, port, cfgv, shape):
+    """PipelineConfig variants (core.hpp:87-112) through the fused path and attention: masks
+    bit-exact outside the epsilon band, attention within the bf16 bars on the same plan; includes
+    non-power-of-two GQA (6 Q / 3 KV heads), ragged L and a single partial block (L = 100)."""
+    Z, Hq, Hkv, L = shape
+    q, k, v = (bf16_round(x) for x in composite_np(41 + L, Z, Hq, Hkv, L))
+    cfg = fp.PipelineConfig(**cfgv)
+    tau = float(cfg.resolved_scale(128))
+    eps = cfgv.get("epsilon", 1e-10)
+    kk = np.repeat(k, Hq // Hkv, axis=1)  # the oracle has no GQA: per-Q-head K (SURVEY §8c)
+    vv = np.repeat(v, Hq // Hkv, axis=1)
+    _, _, sc = port.discover(q, kk, 128, tau, eps)
+    mask, _ = port.max_threshold_mask(sc, 128, cfg.alpha, cfg.sink_tokens, cfg.window_tokens)
+    plan, _, gmask = fp.discover_select(_cuda(q), _cuda(k), cfg, want_mask=True)
+    bad, near, flipped = compare_masks(_np(gmask.active), mask, sc, cfg.alpha)
+    assert bad == 0, (bad, near, flipped)
+    gi, gc = _np(plan.indices), _np(plan.counts)
+    ro, rl, _ = port.block_sparse_attention(q, kk, vv, gi, gc, 128, tau)
+    res = fp.block_sparse_attention(_cuda(q), _cuda(k), _cuda(v), plan,
+                                    fp.make_block_grid(L, 128), tau, out_dtype=torch.float32)
+    _attn_check(_np(res.out), _np(res.lse), ro, rl)
+
+
 # --------------------------------------------------------------------------- attention (K4/K5)
 def _attn_check(go, gl, ro, rl):
     mx, mean = err(go, ro)

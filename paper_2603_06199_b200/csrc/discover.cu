@@ -44,6 +44,7 @@ struct DiscParams {
   DiscoverOut out;
   int* sched;      // zeroed work counter
   int num_items;
+  int prefilled;   // idx rows already hold the fill value N (launch_fill_plan)
   float* mscratch;  // per-CTA m/S rows in global memory when they do not fit in shared memory
 };
 
@@ -70,6 +71,30 @@ __device__ __forceinline__ void decode_item(const Dims& D, int item, int& z, int
   z = t / D.Mr;
 }
 
+#ifdef FPB_TRACE
+// cycle accounting (tools/trace_discover.py): per-thread accumulators, lane 0 of each warp flushes
+__device__ unsigned long long g_dtrace[24];
+#define DT_DECL unsigned long long dt_acc[24] = {}; long long _dt = 0
+#define DT_T0() _dt = clock64()
+#define DT_ADD(i)                                \
+  do {                                           \
+    const long long _n = clock64();              \
+    dt_acc[i] += (unsigned long long)(_n - _dt); \
+    _dt = _n;                                    \
+  } while (0)
+#define DT_FLUSH()                                                         \
+  do {                                                                     \
+    if (lane_id() == 0)                                                    \
+      for (int _i = 0; _i < 24; ++_i)                                      \
+        if (dt_acc[_i]) atomicAdd(&g_dtrace[_i], dt_acc[_i]);              \
+  } while (0)
+#else
+#define DT_DECL
+#define DT_T0()
+#define DT_ADD(i)
+#define DT_FLUSH()
+#endif
+
 template <int NQ>
 __global__ void __launch_bounds__(kThreads, 1)
     discover_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kb,
@@ -82,6 +107,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const Dims& D = prm.D;
 
   const uint32_t warp = warp_id(), lane = lane_id();
+  DT_DECL;
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tm_q);
@@ -116,8 +142,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       int gc = 0;  // global chunk counter (same sequence as the MMA issuer)
       for (int t = 0;; ++t) {
         const int slot = t % kItemRing;
+        DT_T0();
         if (t >= kItemRing) mbar_wait(smem_u32(&s.it_empty[slot]), ((t / kItemRing) - 1) & 1);
+        DT_ADD(12);  // producer: item ring full (epilogue behind)
         int item = atomicAdd(prm.sched, 1);
+        DT_ADD(15);  // producer: work-counter atomic
         if (item >= prm.num_items) item = -1;
         s.items[slot] = item;
         mbar_arrive(smem_u32(&s.it_full[slot]));
@@ -132,7 +161,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         decode_item(D, item, z, h, I);
         const int zkv = z * D.Hkv + h / D.group;
         const int qb = t % kQBuf;
+        DT_T0();
         if (t >= kQBuf) mbar_wait(smem_u32(&s.q_empty[qb]), ((t / kQBuf) - 1) & 1);
+        DT_ADD(13);  // producer: Q buffer busy (MMA behind)
         const uint32_t qf = smem_u32(&s.q_full[qb]);
         mbar_arrive_expect_tx(qf, NQ * kTile);
         for (int p = 0; p < NQ; ++p)
@@ -142,7 +173,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nchunks = I / kBlock + 1;
         for (int c = 0; c < nchunks; ++c, ++gc) {
           const int st = gc % kStages;
+          DT_T0();
           if (gc >= kStages) mbar_wait(smem_u32(&s.kb_empty[st]), ((gc / kStages) - 1) & 1);
+          DT_ADD(14);  // producer: k̄ ring full
           const uint32_t fb = smem_u32(&s.kb_full[st]);
           mbar_arrive_expect_tx(fb, 2 * kTile);
           for (int sp = 0; sp < 2; ++sp)
@@ -166,13 +199,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         int z, h, I;
         decode_item(D, item, z, h, I);
         const int qb = t % kQBuf, wg = t & 1;
+        DT_T0();
         mbar_wait(smem_u32(&s.q_full[qb]), (t / kQBuf) & 1);
+        DT_ADD(8);  // MMA: waiting for Q
         const int nchunks = I / kBlock + 1;
         for (int c = 0; c < nchunks; ++c, ++gc, ++dcw[wg]) {
           const int dc = dcw[wg];
           const int st = gc % kStages, buf = wg * 2 + (dc & 1);
+          DT_T0();
           if (dc >= 2) mbar_wait(smem_u32(&s.d_empty[buf]), ((dc >> 1) - 1) & 1);
+          DT_ADD(9);  // MMA: waiting for the accumulator (epilogue behind)
           mbar_wait(smem_u32(&s.kb_full[st]), (gc / kStages) & 1);
+          DT_ADD(10);  // MMA: waiting for the k̄ chunk
           tc_fence_after();
           const uint32_t d_tmem = tmem + buf * 128;
 #pragma unroll
@@ -190,6 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           mma_commit(smem_u32(&s.kb_empty[st]));
           mma_commit(smem_u32(&s.d_full[buf]));
+          DT_ADD(11);  // MMA: issue
         }
         mma_commit(smem_u32(&s.q_empty[qb]));
       }
@@ -218,7 +257,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int dc = 0;
     for (int t = wg;; t += 2) {
       const int slot = t % kItemRing;
+      DT_T0();
       mbar_wait(smem_u32(&s.it_full[slot]), (t / kItemRing) & 1);
+      DT_ADD(5);  // epilogue: waiting for an item
       const int item = s.items[slot];
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&s.it_empty[slot]));
@@ -232,7 +273,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---- per chunk: TMEM row J -> (local max m, energy S)  (discovery.hpp:96-110)
       for (int c = 0; c < nchunks; ++c, ++dc) {
         const int buf = wg * 2 + (dc & 1);
+        DT_T0();
         mbar_wait(smem_u32(&s.d_full[buf]), (dc >> 1) & 1);
+        DT_ADD(0);  // epilogue: waiting for the accumulator
         tc_fence_after();
         const int J = c * kBlock + et;
         const bool warp_live = c * kBlock + w4 * 32 <= I;  // warp-uniform
@@ -245,6 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(base + 64, *reinterpret_cast<uint32_t(*)[32]>(&v[64]));
           tmem_ld32(base + 96, *reinterpret_cast<uint32_t(*)[32]>(&v[96]));
           tmem_ld_wait();
+          DT_ADD(1);  // epilogue: TMEM load
           // TMEM is in registers: release the accumulator to the MMA warp right away
           tc_fence_before();
           __syncwarp();
@@ -303,7 +347,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           S_s[J] = S;
           tmax = fmaxf(tmax, m);
         }
+        DT_ADD(2);  // epilogue: per-chunk max / exp2 / sums
       }
+      DT_T0();
 
       // ---- outputs: energy / local_max rows (thread-owned J), then normalisation
       const size_t map_row = (((size_t)z * D.Hq + h) * D.M + I) * (size_t)N;
@@ -318,6 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int o = 16; o > 0; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
         if (lane == 0) red[0][w4] = tmax;
         named_bar_sync(ebar, kEpiThreads);
+        DT_ADD(3);  // epilogue: first barrier (warps of the item wait for its slowest warp)
         const float rmax = fmaxf(fmaxf(red[0][0], red[0][1]), fmaxf(red[0][2], red[0][3]));
         // S'_J = S_J exp2(m_J - M_I); total = sum S'; max S' (for the threshold) in one round
         float total = 0.f, pmax = 0.f;
@@ -339,6 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         total = (red[1][0] + red[1][1]) + (red[1][2] + red[1][3]);
         pmax = fmaxf(fmaxf(red[2][0], red[2][1]), fmaxf(red[2][2], red[2][3]));
         const float inv = __fdiv_rn(1.0f, __fadd_rn(total, D.eps));  // discovery.hpp:141-142
+        DT_ADD(16);  // epilogue: rescaled energies, second barrier
         if (prm.out.score)
           for (int J = et; J < N; J += kEpiThreads)
             prm.out.score[map_row + J] = (J <= I) ? __fmul_rn(S_s[J], inv) : 0.f;
@@ -363,6 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (prm.out.mask && J < N) prm.out.mask[(plan_row + J) * D.Hq + h] = act ? 1 : 0;
           }
           named_bar_sync(ebar, kEpiThreads);
+          DT_ADD(17);  // epilogue: threshold, ballots, third barrier
           int base = 0;
           for (int c = 0; c < nchunks; ++c) {
             const int J = c * kBlock + et;
@@ -375,18 +424,21 @@ __global__ void __launch_bounds__(kThreads, 1)
               prm.out.idx[(plan_row + before + __popc(bal & ((1u << lane) - 1u))) * D.Hq + h] = J;
             base += (ired[c * 4 + 0] + ired[c * 4 + 1]) + (ired[c * 4 + 2] + ired[c * 4 + 3]);
           }
+          DT_ADD(18);  // epilogue: compaction (active idx stores)
           if (prm.out.mask)
             for (int J = nchunks * kBlock + et; J < N; J += kEpiThreads)
               prm.out.mask[(plan_row + J) * D.Hq + h] = 0;
-          if (prm.out.idx)
+          if (prm.out.idx && !prm.prefilled)
             for (int slot_j = base + et; slot_j < N; slot_j += kEpiThreads)
               prm.out.idx[(plan_row + slot_j) * D.Hq + h] = N;
           if (prm.out.counts && et == 0)
             prm.out.counts[((size_t)z * D.M + I) * D.Hq + h] = base;
         }
       }
+      DT_ADD(4);  // epilogue: fill + counts
     }
   }
+  DT_FLUSH();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<512>(tmem);
@@ -442,8 +494,28 @@ cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_
     return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(sched, 0, sizeof(int), s);
   if (e != cudaSuccess) return e;
-  DiscParams prm{D, out, sched, D.Z * D.Hq * D.Mr, mscratch};
+  // Long rows: the fill value N of the unused plan slots goes in first as coalesced 16-byte
+  // stores (at 256K, one 4-byte store per slot at stride Hq from the epilogue costs as much as
+  // the compaction itself); short rows keep the in-epilogue fill (a second launch costs more).
+  const int prefilled = out.idx != nullptr && D.M >= 1024 && (D.M * D.Hq) % 4 == 0 &&
+                        reinterpret_cast<uintptr_t>(out.idx) % 16 == 0;
+  if (prefilled) {
+    cudaError_t e = launch_fill_plan(D, out.idx, s);
+    if (e != cudaSuccess) return e;
+  }
+  DiscParams prm{D, out, sched, D.Z * D.Hq * D.Mr, prefilled, mscratch};
   return q_splits == 1 ? launch_nq<1>(D, tm_q, tm_kb, prm, s) : launch_nq<2>(D, tm_q, tm_kb, prm, s);
 }
 
 }  // namespace fpb
+
+#ifdef FPB_TRACE
+extern "C" int fpb_dtrace_read(unsigned long long* host24, int reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(host24, fpb::g_dtrace, sizeof(unsigned long long) * 24);
+  if (reset) {
+    unsigned long long z[24] = {};
+    cudaMemcpyToSymbol(fpb::g_dtrace, z, sizeof(z));
+  }
+  return (int)e;
+}
+#endif

@@ -22,6 +22,8 @@ cudaError_t launch_normalize(const Dims& D, const float* energy, const float* lo
                              float* score, cudaStream_t s);
 cudaError_t launch_threshold(const Dims& D, const float* score, uint8_t* mask,
                              unsigned long long* comparisons, cudaStream_t s);
+// Owned plan rows (Z x [rb + rs k] x N x Hq) set to the fill value N.
+cudaError_t launch_fill_plan(const Dims& D, int32_t* idx, cudaStream_t s);
 cudaError_t launch_compress(const Dims& D, const uint8_t* mask, int32_t* idx, int32_t* counts,
                             cudaStream_t s);
 cudaError_t launch_visit_count(const Dims& D, const int32_t* counts, unsigned long long* total,

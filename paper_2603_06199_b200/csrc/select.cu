@@ -109,6 +109,36 @@ cudaError_t launch_compress(const Dims& D, const uint8_t* mask, int32_t* idx, in
   return cudaGetLastError();
 }
 
+// Plan rows of the owned query blocks set to the fill value N (selection.hpp:176-192), with
+// coalesced 16-byte stores: the fused discovery epilogue then writes only the active slots.
+// Row (z, I) is N * Hq contiguous int32.
+__global__ void fill_plan_kernel(Dims D, int32_t* __restrict__ idx) {
+  const size_t row_ints = (size_t)D.M * D.Hq, row_vec = row_ints / 4;
+  const int rows = D.Z * D.Mr;
+  const int4 f = make_int4(D.M, D.M, D.M, D.M);
+  for (int r = blockIdx.y; r < rows; r += gridDim.y) {
+    const int z = r / D.Mr, I = D.rb + D.rs * (r % D.Mr);
+    int32_t* row = idx + ((size_t)z * D.M + I) * row_ints;
+    int4* row4 = reinterpret_cast<int4*>(row);
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < row_vec;
+         i += (size_t)gridDim.x * blockDim.x)
+      row4[i] = f;
+    for (size_t i = row_vec * 4 + blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < row_ints;
+         i += (size_t)gridDim.x * blockDim.x)
+      row[i] = D.M;
+  }
+}
+
+cudaError_t launch_fill_plan(const Dims& D, int32_t* idx, cudaStream_t s) {
+  if (D.Mr == 0) return cudaSuccess;
+  const size_t row_vec = (size_t)D.M * D.Hq / 4;
+  const int bx = (int)((row_vec + 255) / 256 < 8 ? (row_vec + 255) / 256 : 8);
+  const int rows = D.Z * D.Mr;
+  const dim3 grid(bx < 1 ? 1 : bx, rows < 4096 ? rows : 4096);
+  fill_plan_kernel<<<grid, 256, 0, s>>>(D, idx);
+  return cudaGetLastError();
+}
+
 __global__ void visit_count_kernel(const int32_t* __restrict__ counts, size_t n,
                                    unsigned long long* __restrict__ total) {
   unsigned long long acc = 0;

@@ -94,8 +94,11 @@ def test_compress_arbitrary_mask(fp, port):
 
 @pytest.mark.parametrize("shape", [(1, 2, 2, 2048), (1, 4, 2, 3000), (2, 2, 1, 1024),
                                    (1, 8, 2, 4096)])
-@pytest.mark.parametrize("alpha", [0.05, 0.12, 0.3])
-def test_fused_discover_select(fp, port, shape, alpha):
+@pytest.mark.parametrize("alpha", [0.0, 0.05, 0.12, 0.3])
+@pytest.mark.parametrize("with_maps", [True, False])
+def test_fused_discover_select(fp, port, shape, alpha, with_maps):
+    """with_maps=False is the plan-only hot path (log-domain threshold, two barrier rounds);
+    with_maps=True also writes the score map (linear-domain threshold, three rounds)."""
     Z, Hq, Hkv, L = shape
     q, k, v = composite_np(11 + L, Z, Hq, Hkv, L)
     q, k = bf16_round(q), bf16_round(k)
@@ -104,10 +107,11 @@ def test_fused_discover_select(fp, port, shape, alpha):
     mask, _ = port.max_threshold_mask(sc, 128, alpha, 256, 512)
     idx, counts = port.compress_indices(mask)
     cfg = fp.PipelineConfig(alpha=alpha)
-    plan, smap, gmask = fp.discover_select(_cuda(q), _cuda(k), cfg, want_score=True,
+    plan, smap, gmask = fp.discover_select(_cuda(q), _cuda(k), cfg, want_score=with_maps,
                                            want_mask=True)
     bad, near, flipped = compare_masks(_np(gmask.active), mask, sc, alpha)
-    print(f"shape={shape} alpha={alpha}: near-threshold blocks={near} flipped={flipped}")
+    print(f"shape={shape} alpha={alpha} maps={with_maps}: near-threshold blocks={near} "
+          f"flipped={flipped}")
     assert bad == 0
     ok_rows = ~rows_with_near(sc, alpha)
     gi, gc = _np(plan.indices), _np(plan.counts)

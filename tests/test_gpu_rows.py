@@ -87,3 +87,41 @@ def test_prefill_runner_graph_replay(fp, rows):
         assert torch.equal(r.lse[:, :, sl], ref.lse[:, :, sl])
     # 1 warm-up launch + 3 replays, visits accumulate per launch
     assert visits == 4 * int(plan.counts[:, own].to(torch.int64).sum())
+
+
+def test_one_million_tokens_single_head(fp):
+    """Maximum-size case: L = 2^20 tokens (M = 8192 key blocks, per-key-block rows in the global
+    scratch, plan 256 MiB), one Q / KV head.  Plan invariants of the reference
+    (selection.hpp:176-192) and two full query blocks of the output recomputed in float64 from
+    the plan (attention.hpp:38-132)."""
+    import numpy as np
+    L = 1 << 20
+    q, k, v = fp.workload.composite(17, 1, 1, 1, L, device="cuda")
+    cfg = fp.PipelineConfig(alpha=0.12)
+    grid = fp.make_block_grid(L, 128)
+    tau = cfg.resolved_scale(128)
+    plan = fp.discover_select(q, k, cfg)[0]
+    M = grid.num_query_blocks
+    cnt = plan.counts[0, :, 0]
+    assert bool((cnt >= 1).all()) and bool((cnt <= torch.arange(M, device="cuda") + 1).all())
+    res = fp.block_sparse_attention(q, k, v, plan, grid, tau, out_dtype=torch.float32)
+    assert bool(torch.isfinite(res.out).all()) and bool(torch.isfinite(res.lse).all())
+    for I in (M // 3, M - 1):
+        c = int(cnt[I])
+        blocks = plan.indices[0, I, :c, 0].cpu().numpy()
+        assert np.all(np.diff(blocks) > 0) and blocks[0] == 0 and blocks[-1] == I
+        qi = q[0, 0, I * 128:(I + 1) * 128].double().cpu().numpy()
+        keys = np.concatenate([np.arange(j * 128, (j + 1) * 128) for j in blocks])
+        kk = k[0, 0].double().cpu().numpy()[keys]
+        vv = v[0, 0].double().cpu().numpy()[keys]
+        x = (qi @ kk.T) * tau * np.log2(np.e)
+        rows = np.arange(I * 128, (I + 1) * 128)[:, None]
+        x[keys[None, :] > rows] = -np.inf  # causal mask inside the diagonal block only
+        m = x.max(axis=1, keepdims=True)
+        p = np.exp2(x - m)
+        o = (p @ vv) / p.sum(axis=1, keepdims=True)
+        lse = m[:, 0] + np.log2(p.sum(axis=1))
+        go = res.out[0, 0, I * 128:(I + 1) * 128].double().cpu().numpy()
+        gl = res.lse[0, 0, I * 128:(I + 1) * 128].double().cpu().numpy()
+        assert np.abs(go - o).max() <= 2e-2 and np.abs(go - o).mean() <= 1e-3
+        assert np.abs(gl - lse).max() <= 2e-2

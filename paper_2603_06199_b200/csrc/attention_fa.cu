@@ -206,6 +206,31 @@ __global__ void __launch_bounds__(kThreads, 1)
               nblk += __popc(bal);
             }
             if (lane == 0 && prm.visits && nblk) atomicAdd(prm.visits, (unsigned long long)nblk);
+            if (nblk == 0) {
+              // C = 0 (or only out-of-range slots): out = 0 * (1/0) = NaN, lse = -inf
+              // (attention.hpp:121-125), written here.  An empty item never reaches the other
+              // roles: its softmax warps would release the meta / list buffer before the producer
+              // and the MMA issuer had read it.
+              const int rows = block_len(D, qi);
+              const size_t orow0 = ((size_t)z * D.Hq + h) * (size_t)D.L + (size_t)qi * kBlock;
+              const float nan = __int_as_float(0x7fc00000);
+              const int vec_per_row = prm.out_bf16 ? kHeadDim / 8 : kHeadDim / 4;
+              for (int e = lane; e < rows * vec_per_row; e += 32) {
+                const size_t row = orow0 + e / vec_per_row;
+                const int v4 = e % vec_per_row;
+                if (prm.out_bf16) {
+                  const uint32_t pn = pack_bf16x2(nan, nan);
+                  reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(prm.out) +
+                                           row * kHeadDim)[v4] = make_uint4(pn, pn, pn, pn);
+                } else {
+                  reinterpret_cast<float4*>(reinterpret_cast<float*>(prm.out) +
+                                            row * kHeadDim)[v4] = make_float4(nan, nan, nan, nan);
+                }
+              }
+              for (int r = lane; r < rows; r += 32) prm.lse[orow0 + r] = -INFINITY;
+              __syncwarp();
+              continue;  // fetch another item for this slot; nothing is published
+            }
           }
         }
         __syncwarp();

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -57,8 +58,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#ifdef FPB_WATCHDOG
+  // debug builds: report and trap on a wait that never completes (barrier smem address)
+  long long n = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++n == (1ll << 26)) {
+      printf("watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n", blockIdx.x,
+             threadIdx.x, bar & 0xffffu, parity);
+      asm volatile("trap;");
+    }
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // ---------------------------------------------------------------- fences

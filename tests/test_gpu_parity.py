@@ -279,6 +279,37 @@ def test_attention_edge_semantics(fp, port):
                                   fp.make_block_grid(L, 128), tau)
 
 
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_many_empty_rows_interleaved_with_long_rows(fp, port, out_dtype):
+    """Plans where most rows are empty (C = 0 -> NaN / -inf) between long rows: empty rows are
+    written by the scheduler warp and never become work items, so a fast-finishing empty item
+    cannot release plan-row buffers the producer is still reading (repeated launches)."""
+    Z, H, L = 1, 3, 4096
+    q, k, v = (bf16_round(x) for x in composite_np(13, Z, H, H, L))
+    tau = float(port.scale(128))
+    M = L // 128
+    rng = np.random.default_rng(0)
+    idx = np.full((Z, M, M, H), M, np.int32)
+    counts = np.zeros((Z, M, H), np.int32)
+    for h in range(H):
+        for i in range(M):
+            if rng.random() < 0.3:  # ~30% of rows have work, the rest are empty
+                js = np.sort(rng.choice(i + 1, size=min(i + 1, int(rng.integers(1, 20))),
+                                        replace=False))
+                idx[0, i, :len(js), h] = js
+                counts[0, i, h] = len(js)
+    ro, rl, _ = port.block_sparse_attention(q, k, v, idx, counts, 128, tau)
+    plan = fp.SparseBlockPlan(_cuda(idx, torch.int32), _cuda(counts, torch.int32))
+    for _ in range(5):
+        res = fp.block_sparse_attention(_cuda(q), _cuda(k), _cuda(v), plan,
+                                        fp.make_block_grid(L, 128), tau, out_dtype=out_dtype)
+        go, gl = _np(res.out), _np(res.lse)
+        assert np.array_equal(np.isnan(go), np.isnan(ro))
+        assert np.array_equal(np.isneginf(gl), np.isneginf(rl))
+        fin = ~np.isnan(ro)
+        assert np.abs(go[fin] - ro[fin]).max() <= OUT_MAX_ABS
+
+
 def test_fp32_pipeline_c1_small(fp, port):
     """fp32 inputs (config C1 style, reduced L): discovery split-precision + attention."""
     L = 2048

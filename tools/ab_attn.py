@@ -48,10 +48,13 @@ def main():
         q, k, v = cache[L]
         grid = fp.make_block_grid(L, 128)
         tau = 1 / math.sqrt(D)
-        plan = fp.discover_select(q, k, fp.PipelineConfig(alpha=a))[0]
-        td = timed(lambda: fp.discover_select(q, k, fp.PipelineConfig(alpha=a)), reps=3, warm=1)
+        # device time of each stage from CUDA-graph replays (no host work in the timed region)
+        r = fp.PrefillRunner(q, k, v, fp.PipelineConfig(alpha=a)).capture()
+        td = timed(r.replay_discover, reps=3, warm=1)
+        t = timed(r.replay_attend, reps=3, warm=1)
+        r.check()
+        plan = r.plan
         fl, visits = plan_flops(plan, grid.num_query_blocks)
-        t = timed(lambda: fp.block_sparse_attention(q, k, v, plan, grid, tau), reps=3, warm=1)
         rec = dict(tag=args.tag, L=L, alpha=a, visits=visits, disc_ms=td, attn_ms=t,
                    tflops=fl / t / 1e9, ns_per_visit=t * 1e6 / visits)
         if L in dense_L:

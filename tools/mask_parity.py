@@ -88,9 +88,35 @@ def main():
             flip += int((diff & nearm).sum())
             bad += int((diff & ~nearm).sum())
             bad_rows += int(((diff.any(1)) & ~nearm.any(1)).sum())
+        # attention output on the GPU plan vs float64 for sampled (head, query block) rows
+        grid = fp.make_block_grid(L, B)
+        v = workload.composite(1234, 1, 32, 4, L, device="cuda")[2]
+        res = fp.block_sparse_attention(q, k, v, plan, grid, tau, out_dtype=torch.float32)
+        gen = torch.Generator().manual_seed(L)
+        errs, lerrs = [], []
+        for _ in range(16):
+            h = int(torch.randint(0, 32, (1,), generator=gen))
+            I = int(torch.randint(0, M, (1,), generator=gen))
+            blocks = gi[I, :int(gc[I, h]), h].long()
+            keys = torch.cat([torch.arange(j * B, min(L, (j + 1) * B)) for j in blocks.tolist()])
+            keys = keys.to(q.device)
+            qi = q[0, h, I * B:min(L, (I + 1) * B)].double()
+            x = (qi @ k[0, h // 8, keys].double().T) * tau * math.log2(math.e)
+            rows = torch.arange(I * B, I * B + qi.shape[0], device=q.device)[:, None]
+            x = x.masked_fill(keys[None, :] > rows, -math.inf)  # causal inside the diagonal
+            mx = x.max(1, keepdim=True).values
+            pr = torch.exp2(x - mx)
+            o = (pr @ v[0, h // 8, keys].double()) / pr.sum(1, keepdim=True)
+            lse = mx[:, 0] + torch.log2(pr.sum(1))
+            errs.append((res.out[0, h, I * B:I * B + qi.shape[0]].double() - o).abs())
+            lerrs.append((res.lse[0, h, I * B:I * B + qi.shape[0]].double() - lse).abs())
+        e = torch.cat([x.flatten() for x in errs])
+        le = torch.cat(lerrs)
         rec = dict(L=L, heads=32, alpha=args.alpha, eps_band=EPS_BAND, causal_blocks=tot,
                    near_threshold=near, flipped_in_band=flip, mismatches_outside_band=bad,
-                   plan_rows_differing_without_near_blocks=bad_rows)
+                   plan_rows_differing_without_near_blocks=bad_rows,
+                   attn_sampled_blocks=16, out_max_abs=float(e.max()), out_mean_abs=float(e.mean()),
+                   lse_max_abs=float(le.max()), lse_mean_abs=float(le.mean()))
         line = json.dumps(rec)
         print(line, flush=True)
         if out:

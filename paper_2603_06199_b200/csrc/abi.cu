@@ -141,21 +141,24 @@ size_t ws_discover(const Dims& D, fpb_dtype t) {
     return align_up(pooled_bytes(D)) + 3 * align_up(map_elems(D) * 4) + align_up(map_elems(D));
   size_t b = kSchedBytes + align_up(kbar_split_bytes(D)) + align_up(discover_scratch_bytes(D));
   if (t == FPB_F32) b += align_up(2 * q_elems(D) * 2);
-  return b;
+  return b + (D.M < 1024 ? align_up(discover_rows_bytes(D)) : 0);  // two-pass plan-only mode
 }
 struct DiscWs {
   int* sched;
   __nv_bfloat16* kbar;
   float* mscratch;         // long sequences only (discover_scratch_bytes)
   __nv_bfloat16* qplanes;  // fp32 inputs only
+  float2* rows;            // two-pass plan-only mode (discover_rows_bytes)
 };
-DiscWs disc_ws(const Dims& D, void* ws) {
+DiscWs disc_ws(const Dims& D, void* ws, fpb_dtype t = FPB_BF16) {
   uint8_t* w = static_cast<uint8_t*>(ws);
   const size_t o1 = kSchedBytes + align_up(kbar_split_bytes(D));
   const size_t sb = discover_scratch_bytes(D);
+  const size_t o2 = o1 + align_up(sb);
+  const size_t o3 = o2 + (t == FPB_F32 ? align_up(2 * q_elems(D) * 2) : 0);
   return {reinterpret_cast<int*>(w), reinterpret_cast<__nv_bfloat16*>(w + kSchedBytes),
           sb ? reinterpret_cast<float*>(w + o1) : nullptr,
-          reinterpret_cast<__nv_bfloat16*>(w + o1 + align_up(sb))};
+          reinterpret_cast<__nv_bfloat16*>(w + o2), reinterpret_cast<float2*>(w + o3)};
 }
 // attention: [sched][plan-row scratch] + fp32: Q hi/lo, K hi/lo, V bf16
 size_t ws_attention(const Dims& D, fpb_dtype t) {
@@ -167,6 +170,10 @@ size_t ws_attention(const Dims& D, fpb_dtype t) {
 }
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+#ifndef FPB_DISC_TWO_PASS
+#define FPB_DISC_TWO_PASS 1  // plan-only discovery as kernel + warp-per-row select kernel
+#endif
 
 int need_ws(size_t have, size_t need, void* ws) {
   if (need && (!ws || have < need))
@@ -261,7 +268,7 @@ int fpb_approx_block_scores(const fpb_problem* p, fpb_dtype dtype, const void* Q
     return FPB_OK;
   }
   if ((rc = need_ws(workspace_bytes, ws_discover(D, dtype), workspace))) return rc;
-  const DiscWs w = disc_ws(D, workspace);
+  const DiscWs w = disc_ws(D, workspace, dtype);
   FPB_CUDA(launch_split_pooled(D, pooled, w.kbar, S(stream)));
   const __nv_bfloat16* qp = static_cast<const __nv_bfloat16*>(Q);
   if (dtype == FPB_F32) {
@@ -322,7 +329,7 @@ static int discover_select_rows(const fpb_problem* p, int32_t row_begin, int32_t
     return FPB_OK;
   }
   if (D.Mr == 0) return FPB_OK;  // this row shard owns no query block
-  const DiscWs w = disc_ws(D, workspace);
+  const DiscWs w = disc_ws(D, workspace, dtype);
   const __nv_bfloat16* qp;
   if ((rc = discover_prepare(D, dtype, Q, K, nullptr, w, S(stream), &qp))) return rc;
   DiscoverOut o;
@@ -332,6 +339,10 @@ static int discover_select_rows(const fpb_problem* p, int32_t row_begin, int32_t
   o.mask = mask;
   o.idx = idx;
   o.counts = counts;
+  // plan-only calls (the hot path) up to 128K tokens: two passes, the discovery kernel keeps no
+  // per-item tail (32K: 0.133 -> 0.126 ms; no gain for longer rows, profiles/r1_ab_disc_two_pass)
+  if (FPB_DISC_TWO_PASS && D.M < 1024 && idx && !energy && !local_max && !score && !mask)
+    o.rows = w.rows;
   FPB_CUDA(launch_discover(D, dtype == FPB_F32 ? 2 : 1, qp, w.kbar, o, w.sched, w.mscratch,
                            S(stream)));
   return FPB_OK;

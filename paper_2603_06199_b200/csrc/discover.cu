@@ -343,12 +343,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) mbar_arrive(smem_u32(&s.d_empty[buf]));
         }
         if (J <= I) {
-          m_s[J] = m;
-          S_s[J] = S;
-          tmax = fmaxf(tmax, m);
+          if (prm.out.rows) {  // two-pass mode: coalesced (m, S) pairs, the select kernel does the rest
+            prm.out.rows[((size_t)z * D.Hq + h) * ((size_t)D.M * (D.M + 1) / 2) +
+                         (size_t)I * (I + 1) / 2 + J] = make_float2(m, S);
+          } else {
+            m_s[J] = m;
+            S_s[J] = S;
+            tmax = fmaxf(tmax, m);
+          }
         }
         DT_ADD(2);  // epilogue: per-chunk max / exp2 / sums
       }
+      if (prm.out.rows) continue;  // no per-item tail in two-pass mode
       DT_T0();
 
       // ---- outputs: energy / local_max rows (thread-owned J), then normalisation
@@ -504,7 +510,9 @@ cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_
     if (e != cudaSuccess) return e;
   }
   DiscParams prm{D, out, sched, D.Z * D.Hq * D.Mr, prefilled, mscratch};
-  return q_splits == 1 ? launch_nq<1>(D, tm_q, tm_kb, prm, s) : launch_nq<2>(D, tm_q, tm_kb, prm, s);
+  e = q_splits == 1 ? launch_nq<1>(D, tm_q, tm_kb, prm, s) : launch_nq<2>(D, tm_q, tm_kb, prm, s);
+  if (e != cudaSuccess || !out.rows) return e;
+  return launch_select_rows(D, out.rows, out.idx, out.counts, prefilled != 0, s);
 }
 
 }  // namespace fpb

@@ -39,7 +39,17 @@ struct DiscoverOut {
   int32_t* idx = nullptr;
   int32_t* counts = nullptr;
   bool normalize = true;  // false: only energy/local_max (approx_block_scores)
+  // Two-pass plan-only mode: the discovery kernel writes the causal (local max, energy) pairs
+  // of every row to `rows` (packed triangle per (z, h): row I at I(I+1)/2) and a warp-per-row
+  // select kernel normalises, thresholds and compacts them (select.cu).
+  float2* rows = nullptr;
 };
+// Bytes of the packed (m, S) triangle of the two-pass mode.
+inline size_t discover_rows_bytes(const Dims& D) {
+  return (size_t)D.Z * D.Hq * ((size_t)D.M * (D.M + 1) / 2) * sizeof(float2);
+}
+cudaError_t launch_select_rows(const Dims& D, const float2* rows, int32_t* idx, int32_t* counts,
+                               bool prefilled, cudaStream_t s);
 cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_planes,
                             const __nv_bfloat16* kbar_split, const DiscoverOut& out, int* sched,
                             float* mscratch, cudaStream_t s);

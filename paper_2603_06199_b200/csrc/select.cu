@@ -129,6 +129,67 @@ __global__ void fill_plan_kernel(Dims D, int32_t* __restrict__ idx) {
   }
 }
 
+// Two-pass plan-only discovery, second pass: one warp per owned (z, h, I) row of the packed
+// (local max, energy) triangle.  normalize_block_scores (discovery.hpp:131-143), the max-based
+// threshold with sink / window retention (selection.hpp:63-92) and compress_indices
+// (selection.hpp:176-192) in three sweeps over the row (L1/L2-resident after the first).
+__global__ void select_rows_kernel(Dims D, const float2* __restrict__ rows,
+                                   int32_t* __restrict__ idx, int32_t* __restrict__ counts,
+                                   int prefilled) {
+  const long wrow = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long nrows = (long)D.Z * D.Hq * D.Mr;
+  if (wrow >= nrows) return;
+  const int lane = threadIdx.x & 31;
+  const int h = (int)(wrow % D.Hq);
+  const long t = wrow / D.Hq;
+  const int I = owned_row(D, (int)(t % D.Mr));
+  const int z = (int)(t / D.Mr);
+  const int N = D.M;
+  const float2* r = rows + ((size_t)z * D.Hq + h) * ((size_t)D.M * (D.M + 1) / 2) +
+                    (size_t)I * (I + 1) / 2;
+  float rmax = kNegSentinel;
+  for (int J = lane; J <= I; J += 32) rmax = fmaxf(rmax, r[J].x);
+  rmax = warp_max(rmax);
+  float total = 0.f, pmax = 0.f;
+  for (int J = lane; J <= I; J += 32) {
+    const float2 ms = r[J];
+    const float sp = __fmul_rn(ms.y, exp2f(__fsub_rn(ms.x, rmax)));
+    total += sp;
+    pmax = fmaxf(pmax, sp);
+  }
+  total = warp_sum(total);
+  pmax = warp_max(pmax);
+  const float inv = __fdiv_rn(1.0f, __fadd_rn(total, D.eps));
+  // max_J fl(S'_J inv) == fl(max_J S'_J * inv) (monotone rounding, inv > 0); max_val >= 0
+  const float thresh = __fmul_rn(D.alpha, __fmul_rn(pmax, inv));
+  const size_t plan_row = ((size_t)z * D.M + I) * (size_t)N;
+  int base = 0;
+  for (int J0 = 0; J0 <= I; J0 += 32) {
+    const int J = J0 + lane;
+    bool act = false;
+    if (J <= I) {
+      const float2 ms = r[J];
+      const float sc = __fmul_rn(__fmul_rn(ms.y, exp2f(__fsub_rn(ms.x, rmax))), inv);
+      act = sc >= thresh || J < D.sink_blocks || (I - J) < D.window_blocks;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, act);
+    if (act) idx[(plan_row + base + __popc(bal & ((1u << lane) - 1u))) * D.Hq + h] = J;
+    base += __popc(bal);
+  }
+  if (!prefilled)
+    for (int slot = base + lane; slot < N; slot += 32) idx[(plan_row + slot) * D.Hq + h] = N;
+  if (lane == 0) counts[((size_t)z * D.M + I) * D.Hq + h] = base;
+}
+
+cudaError_t launch_select_rows(const Dims& D, const float2* rows, int32_t* idx, int32_t* counts,
+                               bool prefilled, cudaStream_t s) {
+  const long nrows = (long)D.Z * D.Hq * D.Mr;
+  if (nrows == 0) return cudaSuccess;
+  select_rows_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, s>>>(D, rows, idx, counts,
+                                                                  prefilled ? 1 : 0);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill_plan(const Dims& D, int32_t* idx, cudaStream_t s) {
   if (D.Mr == 0) return cudaSuccess;
   const size_t row_vec = (size_t)D.M * D.Hq / 4;

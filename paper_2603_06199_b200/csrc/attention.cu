@@ -14,6 +14,8 @@
 //   w2  TMEM allocator (512 cols: S0 | S1 | O)
 //   w4..w7 softmax    thread = query row = TMEM lane: rowmax, lazy rescale (FA4-style, only when
 //                     the max grows by > 2^8), exp2, P (bf16) written back over S_b in TMEM.
+#include <cstdlib>
+
 #include "fp_kernels.h"
 
 namespace fpb {
@@ -361,9 +363,17 @@ cudaError_t launch_attention(const Dims& D, int splits, const __nv_bfloat16* Q,
                              const int32_t* counts, bool out_bf16, void* out, float* lse,
                              unsigned long long* visits, int32_t* plan_error, int* sched,
                              uint16_t* lists, cudaStream_t s) {
-  if (splits == 1)
+  if (splits == 1) {
+    static const bool fa2 = [] {
+      const char* e = std::getenv("FPB_FA2");
+      return e && e[0] == '1';
+    }();
+    if (fa2)
+      return launch_attention_fa2(D, Q, K, V, idx, counts, out_bf16, out, lse, visits, plan_error,
+                                  sched, lists, s);
     return launch_attention_fa(D, Q, K, V, idx, counts, out_bf16, out, lse, visits, plan_error,
                                sched, lists, s);
+  }
   CUtensorMap tm_q, tm_k, tm_v;
   if (!make_tmap_rows128(&tm_q, Q, D.L, (uint64_t)splits * D.Z * D.Hq) ||
       !make_tmap_rows128(&tm_k, K, D.L, (uint64_t)splits * D.Z * D.Hkv) ||

@@ -1,0 +1,649 @@
+// attention_fa3.cu — K4/K5 variant with S accumulated in fp16 and double-buffered per slot.
+//
+// Same persistent two-slot structure as attention_fa.cu.  QK^T accumulates in fp16
+// (.kind::f16 with an f16 D), so S of a 128-key block takes 64 TMEM columns and each slot owns two
+// S buffers next to its O accumulator (2 x 64 + 128 columns per slot).  The MMA issue order per
+// slot is QK(0), QK(1), then PV(n), QK(n+2): QK^T of the next block runs while the softmax works on
+// the current one, so a slot's period is max(softmax, MMA) instead of their sum.  P (bf16) of a
+// block overwrites its own S buffer.  Buffers alternate with the slot's global block count.
+#include <cstdlib>
+#include <cuda_fp16.h>
+
+#include "fp_kernels.h"
+
+namespace fpb {
+
+using namespace ptx;
+
+namespace {
+
+constexpr int kThreads = 384;
+constexpr int kTile = kBlock * kHeadDim * 2;  // 32 KiB bf16 tile
+constexpr int kRing = 5;                      // shared K/V tile ring
+constexpr float kRescaleThreshold = 8.0f;     // lazy O rescale (log2 units)
+#ifndef FPB_POLY_MASK
+#define FPB_POLY_MASK 0  // pairs p with (p & 3) in this bit mask use exp2_poly2 (FMA pipe)
+#endif
+
+struct FaParams {
+  Dims D;
+  const int32_t* idx;  // nullptr -> dense causal
+  const int32_t* counts;
+  void* out;
+  float* lse;
+  unsigned long long* visits;
+  int32_t* plan_error;
+  int* sched;
+  uint16_t* lists;  // global scratch: [grid][2 slots][2 bufs][M] compacted plan rows
+  int num_items;
+  int out_bf16;
+  int gs;     // KV groups per super-group of the work order (divides Hkv)
+};
+
+#ifdef FPB_TRACE
+// cycle accounting (tools/trace_attention.py): per-warp register accumulators, flushed once
+__device__ unsigned long long g_trace3[16];
+#define TR_DECL unsigned long long tr_acc[16] = {}
+#define TR_T0() long long _tr = clock64()
+#define TR_ADD(i)                                  \
+  do {                                             \
+    const long long _n = clock64();                \
+    tr_acc[i] += (unsigned long long)(_n - _tr);   \
+    _tr = _n;                                      \
+  } while (0)
+#define TR_FLUSH()                                                          \
+  do {                                                                      \
+    if (lane_id() == 0)                                                     \
+      for (int _i = 0; _i < 16; ++_i)                                       \
+        if (tr_acc[_i]) atomicAdd(&g_trace3[_i], tr_acc[_i]);                \
+  } while (0)
+#else
+#define TR_DECL
+#define TR_T0()
+#define TR_ADD(i)
+#define TR_FLUSH()
+#endif
+
+struct SlotMeta {
+  int item;  // -1: no more work
+  int nblk;
+};
+
+struct FaSmem {
+  uint8_t q[2][kTile];
+  uint8_t ring[kRing][kTile];
+  uint64_t q_full[2], q_empty[2];
+  uint64_t kv_full[kRing], kv_empty[kRing];
+  // [slot][S buffer]: o_done completes once per PV of that buffer's halves, so every parity wait
+  // is at most one phase behind (two PVs of a slot can be in flight at once)
+  uint64_t s_full[2][2], p_ready[2][2], o_done[2][2], o_free[2];
+  uint64_t meta_full[2][2], meta_empty[2][2];
+  SlotMeta meta[2][2];
+  uint32_t tmem_base;
+};
+
+// Work-item order: (z, KV super-group, query block heavy-first, head within the super-group).
+// A super-group is `gs` adjacent KV groups.  The Q heads of one KV group are adjacent within a
+// query block, so their K/V tiles are fetched once and re-read from L2; `gs` bounds the K/V
+// working set of the ~296 concurrent items to gs groups (chosen on the host so that it stays
+// well inside the 126 MB L2).  gs == Hkv is "all heads fastest" (best while everything fits).
+__device__ __forceinline__ void decode(const Dims& D, int gs, int item, int& z, int& h, int& qi) {
+  const int hs = gs * D.group;
+  const int hh = item % hs;
+  int t = item / hs;
+  qi = owned_row(D, t % D.Mr);  // heavy (long rows) first
+  t /= D.Mr;
+  const int nsg = D.Hkv / gs;
+  h = (t % nsg) * hs + hh;
+  z = t / nsg;
+}
+
+// Per-slot progress shared by the producer's and the MMA issuer's identical unit schedules.
+struct SlotState {
+  int t = 0;      // items taken by this slot (incl. empty ones and the final sentinel)
+  int j = 0;      // step within the current item (0 .. 2 nblk + 1)
+  int nblk = 0;
+  int item = 0;
+  int qc = 0;     // items with nblk > 0 (Q loads / O lifetimes)
+  int pc[2] = {0, 0};  // P blocks consumed per S buffer (p_ready phases)
+  int gb = 0;          // blocks of all previous items: block n uses S buffer (gb + n) & 1
+  bool active = true;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    fa3_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+              const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+              const FaParams prm) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  auto& s = *reinterpret_cast<FaSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                       ~uintptr_t(1023));
+  const Dims& D = prm.D;
+  const int N = D.M;
+  uint16_t* lists = prm.lists + (size_t)blockIdx.x * 4 * D.M;
+  auto list_of = [&](int slot, int p) { return lists + (size_t)(slot * 2 + p) * D.M; };
+  const bool dense = prm.idx == nullptr;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  TR_DECL;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_o);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&s.q_full[i]), 1);
+      mbar_init(smem_u32(&s.q_empty[i]), 1);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(smem_u32(&s.s_full[i][b]), 1);
+        mbar_init(smem_u32(&s.p_ready[i][b]), 4);
+        mbar_init(smem_u32(&s.o_done[i][b]), 1);
+      }
+      mbar_init(smem_u32(&s.o_free[i]), 4);
+      for (int p = 0; p < 2; ++p) {
+        mbar_init(smem_u32(&s.meta_full[i][p]), 1);
+        mbar_init(smem_u32(&s.meta_empty[i][p]), 4);
+      }
+    }
+    for (int i = 0; i < kRing; ++i) {
+      mbar_init(smem_u32(&s.kv_full[i]), 1);
+      mbar_init(smem_u32(&s.kv_empty[i]), 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(smem_u32(&s.tmem_base));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s.tmem_base;
+  // 384 threads x 168 regs at launch; hand the control warpgroup's share to the softmax WGs
+  if (warp < 4) {
+  setmaxnreg_dec<72>();
+  if (warp == 3) {
+    // ===================== scheduler: fetch items, compact plan rows, publish per-slot metas
+    // (runs up to two items ahead per slot so plan-row loads never stall the TMA producer)
+    int t[2] = {0, 0};
+    bool done[2] = {false, false};
+    while (!done[0] || !done[1]) {
+      for (int sl = 0; sl < 2; ++sl) {
+        if (done[sl]) continue;
+        const int p = t[sl] & 1;
+        if (t[sl] >= 2) {
+          const bool ready = mbar_try_wait(smem_u32(&s.meta_empty[sl][p]), ((t[sl] >> 1) - 1) & 1);
+          if (!__shfl_sync(0xffffffffu, ready, 0)) continue;
+        }
+        __syncwarp();
+        int item = 0;
+        if (lane == 0) item = atomicAdd(prm.sched, 1);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= prm.num_items) item = -1;
+        int nblk = 0;
+        if (item >= 0) {
+          int z, h, qi;
+          decode(D, prm.gs, item, z, h, qi);
+          if (dense) {
+            nblk = qi + 1;
+          } else {
+            const int C = prm.counts[((size_t)z * D.M + qi) * D.Hq + h];
+            const size_t prow = ((size_t)z * D.M + qi) * (size_t)N;
+            uint16_t* lst = list_of(sl, p);
+            for (int s0 = 0; s0 < C; s0 += 32) {  // attention.hpp:76-81: range-check each slot
+              const int slot = s0 + lane;
+              int bid = -1;
+              if (slot < C) bid = prm.idx[(prow + slot) * D.Hq + h];
+              const bool ok = slot < C && bid >= 0 && bid < N;
+              if (slot < C && !ok && prm.plan_error) atomicExch(prm.plan_error, 1);
+              const unsigned bal = __ballot_sync(0xffffffffu, ok);
+              if (ok) lst[nblk + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)bid;
+              nblk += __popc(bal);
+            }
+            if (lane == 0 && prm.visits && nblk) atomicAdd(prm.visits, (unsigned long long)nblk);
+            if (nblk == 0) {
+              // C = 0 (or only out-of-range slots): out = 0 * (1/0) = NaN, lse = -inf
+              // (attention.hpp:121-125), written here.  An empty item never reaches the other
+              // roles: its softmax warps would release the meta / list buffer before the producer
+              // and the MMA issuer had read it.
+              const int rows = block_len(D, qi);
+              const size_t orow0 = ((size_t)z * D.Hq + h) * (size_t)D.L + (size_t)qi * kBlock;
+              const float nan = __int_as_float(0x7fc00000);
+              const int vec_per_row = prm.out_bf16 ? kHeadDim / 8 : kHeadDim / 4;
+              for (int e = lane; e < rows * vec_per_row; e += 32) {
+                const size_t row = orow0 + e / vec_per_row;
+                const int v4 = e % vec_per_row;
+                if (prm.out_bf16) {
+                  const uint32_t pn = pack_bf16x2(nan, nan);
+                  reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(prm.out) +
+                                           row * kHeadDim)[v4] = make_uint4(pn, pn, pn, pn);
+                } else {
+                  reinterpret_cast<float4*>(reinterpret_cast<float*>(prm.out) +
+                                            row * kHeadDim)[v4] = make_float4(nan, nan, nan, nan);
+                }
+              }
+              for (int r = lane; r < rows; r += 32) prm.lse[orow0 + r] = -INFINITY;
+              __syncwarp();
+              continue;  // fetch another item for this slot; nothing is published
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          s.meta[sl][p].item = item;
+          s.meta[sl][p].nblk = nblk;
+          mbar_arrive(smem_u32(&s.meta_full[sl][p]));
+        }
+        __syncwarp();
+        ++t[sl];
+        if (item < 0) done[sl] = true;
+      }
+    }
+  } else if (warp == 0) {
+    // ===================== TMA producer (whole warp; lane 0 issues)
+    const uint64_t pol_q = policy_evict_first();
+    const uint64_t pol_kv = policy_evict_last();
+    SlotState st[2];
+    int kvc = 0;  // tiles pushed through the ring
+    auto push = [&](const CUtensorMap* map, int row, int plane) {
+      const int r = kvc % kRing;
+      TR_T0();
+      if (kvc >= kRing) mbar_wait(smem_u32(&s.kv_empty[r]), ((kvc / kRing) - 1) & 1);
+      TR_ADD(12);  // producer: waiting for a free ring slot
+      if (lane == 0) {
+        const uint32_t fb = smem_u32(&s.kv_full[r]);
+        mbar_arrive_expect_tx(fb, kTile);
+        for (int a = 0; a < 2; ++a)
+          tma_load_3d_hint(smem_u32(s.ring[r]) + a * (kTile / 2), map, fb, a * 64, row, plane,
+                           pol_kv);
+      }
+      __syncwarp();
+      ++kvc;
+    };
+    while (st[0].active || st[1].active) {
+      for (int sl = 0; sl < 2; ++sl) {
+        SlotState& S = st[sl];
+        if (!S.active) continue;
+        const int p = S.t & 1;
+        if (S.j == 0) {
+          {
+            TR_T0();
+            mbar_wait(smem_u32(&s.meta_full[sl][p]), (S.t >> 1) & 1);
+            TR_ADD(14);  // producer: waiting for the scheduler
+          }
+          S.item = s.meta[sl][p].item;
+          S.nblk = s.meta[sl][p].nblk;
+          if (S.item < 0) {
+            S.active = false;
+            continue;
+          }
+          if (S.nblk == 0) {  // nothing to load; the softmax warps write NaN / -inf
+            ++S.t;
+            continue;
+          }
+          int z, h, qi;
+          decode(D, prm.gs, S.item, z, h, qi);
+          {
+            TR_T0();
+            if (S.qc >= 1) mbar_wait(smem_u32(&s.q_empty[sl]), (S.qc - 1) & 1);
+            TR_ADD(13);  // producer: waiting for the slot's Q tile (previous epilogue)
+          }
+          if (lane == 0) {
+            const uint32_t qb = smem_u32(&s.q_full[sl]);
+            mbar_arrive_expect_tx(qb, kTile);
+            for (int a = 0; a < 2; ++a)
+              tma_load_3d_hint(smem_u32(s.q[sl]) + a * (kTile / 2), &tm_q, qb, a * 64,
+                               qi * kBlock, z * D.Hq + h, pol_q);
+          }
+          __syncwarp();
+          ++S.qc;
+        }
+        // ---- step k = S.j: the MMA issues PV(k-2) then QK(k); tiles are pushed at their first
+        // use: K(0) at step 0, V(n) and K(n+1) at step 2n+2 (odd steps reuse them)
+        int z, h, qi;
+        decode(D, prm.gs, S.item, z, h, qi);
+        const int zkv = z * D.Hkv + h / D.group;
+        const uint16_t* lst = list_of(sl, p);
+        // step k: the MMA issues PV(k-2) then QK(k); every tile is used once
+        const int k = S.j, H = S.nblk;
+        if (k >= 2) push(&tm_v, (dense ? k - 2 : (int)lst[k - 2]) * kBlock, zkv);
+        if (k < H) push(&tm_k, (dense ? k : (int)lst[k]) * kBlock, zkv);
+        if (++S.j == H + 2) {
+          S.j = 0;
+          ++S.t;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer: mirrors the producer's unit schedule
+    const bool leader = elect_one();
+    // QK^T: bf16 x bf16 -> f16 accumulator (D format bits = 0), N = 128
+    // f16 x f16 -> f16 (bf16 inputs only accumulate in f32): D format, A and B type bits = 0.
+    // FPB_FA3_TIMING_ONLY reinterprets the bf16 tiles as f16 (wrong numerics, timing probe).
+    constexpr uint32_t idesc_qk =
+        idesc_bf16_f32(128, 128, false, false) & ~((1u << 4) | (7u << 7) | (7u << 10));
+    constexpr uint32_t idesc_pv = idesc_bf16_f32(128, 128, false, true);
+    SlotState st[2];
+    int kvc = 0;
+    while (st[0].active || st[1].active) {
+      for (int sl = 0; sl < 2; ++sl) {
+        SlotState& S = st[sl];
+        if (!S.active) continue;
+        const int p = S.t & 1;
+        const uint32_t s_tmem = tmem + sl * 128, o_tmem = tmem + 256 + sl * 128;
+        if (S.j == 0) {
+          mbar_wait(smem_u32(&s.meta_full[sl][p]), (S.t >> 1) & 1);
+          S.item = s.meta[sl][p].item;
+          S.nblk = s.meta[sl][p].nblk;
+          if (S.item < 0) {
+            S.active = false;
+            continue;
+          }
+          if (S.nblk == 0) {
+            ++S.t;
+            continue;
+          }
+          {
+            TR_T0();
+            mbar_wait(smem_u32(&s.q_full[sl]), S.qc & 1);
+            TR_ADD(15);  // MMA: waiting for Q
+          }
+          ++S.qc;
+        }
+        const int k = S.j, H = S.nblk;
+        if (k >= 2) {
+          // PV(u), u = k-2: O_sl (+)= P(u) [TMEM, S buffer (gb+u)&1] x V(u) [ring, MN-major]
+          const int u = k - 2, bf = (S.gb + u) & 1;
+          if (u == 0 && S.qc >= 2) mbar_wait(smem_u32(&s.o_free[sl]), (S.qc - 2) & 1);
+          const int rv = kvc % kRing;
+          TR_T0();
+          mbar_wait(smem_u32(&s.kv_full[rv]), (kvc / kRing) & 1);
+          TR_ADD(8);  // MMA: waiting for V
+          ++kvc;
+          const uint32_t vb = smem_u32(s.ring[rv]);
+          TR_T0();
+          mbar_wait(smem_u32(&s.p_ready[sl][bf]), S.pc[bf] & 1);
+          ++S.pc[bf];
+          tc_fence_after();
+          TR_ADD(9);  // MMA: waiting for P
+          if (leader) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              mma_bf16_ts(o_tmem, s_tmem + bf * 64 + ks * 8,
+                          sdesc_sw128(vb + ks * 2048, kTile / 2, 1024), idesc_pv,
+                          (u > 0 || ks > 0) ? 1u : 0u);
+            mma_commit(smem_u32(&s.kv_empty[rv]));
+            mma_commit(smem_u32(&s.o_done[sl][bf]));
+          }
+          __syncwarp();
+        }
+        if (k < H) {
+          // QK(k): S buffer (gb+k)&1 = Q_sl K(k)^T, f16 accumulator (64 packed columns)
+          const int bf = (S.gb + k) & 1;
+          const int rk = kvc % kRing;
+          TR_T0();
+          mbar_wait(smem_u32(&s.kv_full[rk]), (kvc / kRing) & 1);
+          TR_ADD(11);  // MMA: waiting for K
+          ++kvc;
+          tc_fence_after();
+          if (leader) {
+            const uint32_t qb = smem_u32(s.q[sl]), kb = smem_u32(s.ring[rk]);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+              const uint32_t off = (ks >> 2) * (kTile / 2) + (ks & 3) * 32;
+              mma_bf16_ss(s_tmem + bf * 64, sdesc_sw128(qb + off, 16, 1024),
+                          sdesc_sw128(kb + off, 16, 1024), idesc_qk, ks > 0 ? 1u : 0u);
+            }
+            mma_commit(smem_u32(&s.kv_empty[rk]));
+            mma_commit(smem_u32(&s.s_full[sl][bf]));
+          }
+          __syncwarp();
+        }
+        if (++S.j == H + 2) {
+          S.j = 0;
+          S.gb += H;
+          ++S.t;
+        }
+      }
+    }
+  }
+  } else {
+    setmaxnreg_inc<216>();
+    // ===================== softmax + epilogue, one warpgroup per slot
+    const int sl = (warp - 4) >> 2;
+    const int r = ((warp - 4) & 3) * 32 + lane;  // query row == TMEM lane
+    const uint32_t lane_addr = static_cast<uint32_t>(((warp - 4) & 3) * 32) << 16;
+    const uint32_t s_addr = tmem + lane_addr + sl * 128;
+    const uint32_t o_addr = tmem + lane_addr + 256 + sl * 128;
+    int hc = 0, qc = 0;   // blocks processed (global per slot: buffers, o_done phases), Q tiles
+    int sb[2] = {0, 0};   // QK^T blocks consumed per S buffer (s_full phases)
+    for (int t = 0;; ++t) {
+      const int p = t & 1;
+      mbar_wait(smem_u32(&s.meta_full[sl][p]), (t >> 1) & 1);
+      const int item = s.meta[sl][p].item;
+      const int nblk = s.meta[sl][p].nblk;
+      if (item < 0) break;
+      const uint16_t* lst = list_of(sl, p);
+      int z, h, qi;
+      decode(D, prm.gs, item, z, h, qi);
+      const int rows = block_len(D, qi);
+      float m_used = -INFINITY, l = 0.f;
+      for (int n = 0; n < nblk; ++n, ++hc) {
+        const int bf = hc & 1;  // S buffer of this block (global block parity of the slot)
+        const int kv = dense ? n : (int)lst[n];
+        const int cols = block_len(D, kv);
+        const int lim = (kv == qi) ? min(cols, r + 1) : cols;  // attention.hpp:85-91
+        const bool full = __all_sync(0xffffffffu, lim == kBlock);
+        TR_T0();
+        mbar_wait(smem_u32(&s.s_full[sl][bf]), sb[bf] & 1);
+        ++sb[bf];
+        tc_fence_after();
+        TR_ADD(0);  // softmax: waiting for S
+        float x[128];
+        {
+          uint32_t raw[64];
+          tmem_ld64(s_addr + bf * 64, &raw[0]);
+          tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {  // f16 pairs: keys 2c (low half), 2c+1 (high half)
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&raw[c]));
+            x[2 * c] = f.x;
+            x[2 * c + 1] = f.y;
+          }
+        }
+        if (!full) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c >= lim) x[c] = -INFINITY;
+        }
+        float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 128; c += 8) {  // 4 independent 3-input max chains
+          mx0 = fmaxf(mx0, fmaxf(x[c + 0], x[c + 1]));
+          mx1 = fmaxf(mx1, fmaxf(x[c + 2], x[c + 3]));
+          mx2 = fmaxf(mx2, fmaxf(x[c + 4], x[c + 5]));
+          mx3 = fmaxf(mx3, fmaxf(x[c + 6], x[c + 7]));
+        }
+        const float sc = D.to_bits;
+        const float m_new = fmaxf(m_used, fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sc);
+        TR_ADD(1);  // softmax: TMEM load + unpack + mask + row max
+        if (n == 0) {
+          m_used = m_new;
+        } else if (__any_sync(0xffffffffu, m_new > m_used + kRescaleThreshold)) {
+          // lazy O rescale (exact: numerator and denominator share the stale max); O must hold
+          // PV(n-1)
+          mbar_wait(smem_u32(&s.o_done[sl][(hc - 1) & 1]), ((hc - 1) >> 1) & 1);
+          tc_fence_after();
+          const float f = ex2_approx(m_used - m_new);
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            uint32_t o[32];
+            tmem_ld32(o_addr + cc * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * f);
+            tmem_st32(o_addr + cc * 32, o);
+          }
+          l *= f;
+          m_used = m_new;
+        }
+        TR_ADD(2);  // softmax: lazy O rescale (rare)
+        const float neg_m = -m_used;
+        float bs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[64];  // P as bf16 pairs: keys 2c, 2c+1 in column c
+        if (full) {
+#pragma unroll
+          for (int c = 0; c < 128; c += 2) {
+            float x0, x1;
+            ffma2(x0, x1, x[c], x[c + 1], sc, sc, neg_m, neg_m);
+            const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
+            const int a = ((c >> 1) & 3) * 2;
+            fadd2(bs[a], bs[a + 1], bs[a], bs[a + 1], p0, p1);
+            pk[c >> 1] = pack_bf16x2(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 128; c += 2) {
+            const float p0 = ex2_approx(fmaf(x[c], sc, neg_m));
+            const float p1 = ex2_approx(fmaf(x[c + 1], sc, neg_m));
+            const int a = ((c >> 1) & 3) * 2;
+            fadd2(bs[a], bs[a + 1], bs[a], bs[a + 1], p0, p1);
+            pk[c >> 1] = pack_bf16x2(p0, p1);
+          }
+        }
+        tmem_st32(s_addr + bf * 64, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        tmem_st32(s_addr + bf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&s.p_ready[sl][bf]));
+        TR_ADD(3);  // softmax: exp + pack + TMEM store
+        l += ((bs[0] + bs[1]) + (bs[2] + bs[3])) + ((bs[4] + bs[5]) + (bs[6] + bs[7]));
+      }
+      TR_T0();
+      // ---- epilogue (attention.hpp:119-126)
+      const size_t orow = ((size_t)z * D.Hq + h) * (size_t)D.L + (size_t)qi * kBlock + r;
+      if (nblk > 0) {
+        // the last two PVs (one per S buffer) can both still be in flight
+        if (nblk >= 2) mbar_wait(smem_u32(&s.o_done[sl][(hc - 2) & 1]), ((hc - 2) >> 1) & 1);
+        mbar_wait(smem_u32(&s.o_done[sl][(hc - 1) & 1]), ((hc - 1) >> 1) & 1);
+        tc_fence_after();
+        const float inv = 1.0f / l;
+        const uint32_t stage = smem_u32(s.q[sl]);  // this slot's Q tile is free: O staging
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t o[32];
+          tmem_ld32(o_addr + cc * 32, o);
+          tmem_ld_wait();
+          if (cc == 3) {  // O fully read: release the accumulator for the slot's next item
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&s.o_free[sl]));
+          }
+          if (prm.out_bf16) {
+            // row r, columns 32cc..32cc+31 -> SW128 tile layout of the TMA box (64 cols x 128 rows)
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const int col = cc * 32 + q4 * 8;
+              const uint32_t off = (col >> 6) * (kTile / 2) + r * 128 +
+                                   ((((col & 63) >> 3) ^ (r & 7)) << 4);
+              const uint4 val = make_uint4(
+                  pack_bf16x2(__uint_as_float(o[8 * q4 + 0]) * inv, __uint_as_float(o[8 * q4 + 1]) * inv),
+                  pack_bf16x2(__uint_as_float(o[8 * q4 + 2]) * inv, __uint_as_float(o[8 * q4 + 3]) * inv),
+                  pack_bf16x2(__uint_as_float(o[8 * q4 + 4]) * inv, __uint_as_float(o[8 * q4 + 5]) * inv),
+                  pack_bf16x2(__uint_as_float(o[8 * q4 + 6]) * inv, __uint_as_float(o[8 * q4 + 7]) * inv));
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stage + off),
+                           "r"(val.x), "r"(val.y), "r"(val.z), "r"(val.w)
+                           : "memory");
+            }
+          } else if (r < rows) {
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(prm.out) +
+                                                    orow * kHeadDim + cc * 32);
+#pragma unroll
+            for (int q4 = 0; q4 < 8; ++q4)
+              dst[q4] = make_float4(__uint_as_float(o[4 * q4]) * inv,
+                                    __uint_as_float(o[4 * q4 + 1]) * inv,
+                                    __uint_as_float(o[4 * q4 + 2]) * inv,
+                                    __uint_as_float(o[4 * q4 + 3]) * inv);
+          }
+        }
+        if (r < rows) prm.lse[orow] = m_used + log2f(l);
+        if (prm.out_bf16) {
+          fence_proxy_async_smem();
+          named_bar_sync(1 + sl, 128);
+          if (r == 0) {  // rows beyond L are clipped by the tensor map
+            tma_store_3d(&tm_o, stage, 0, qi * kBlock, z * D.Hq + h);
+            tma_store_3d(&tm_o, stage + kTile / 2, 64, qi * kBlock, z * D.Hq + h);
+            bulk_commit();
+            bulk_wait_read0();
+            mbar_arrive(smem_u32(&s.q_empty[sl]));
+          }
+        } else {
+          named_bar_sync(1 + sl, 128);  // every thread is past its tcgen05.ld of O
+          if (r == 0) mbar_arrive(smem_u32(&s.q_empty[sl]));
+        }
+        ++qc;
+      } else if (r < rows) {  // C = 0: out = 0 * (1/0) = NaN, lse = -inf (attention.hpp:121-125)
+        const float nan = __int_as_float(0x7fc00000);
+        if (prm.out_bf16) {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(prm.out) + orow * kHeadDim);
+          const uint32_t pn = pack_bf16x2(nan, nan);
+          for (int q4 = 0; q4 < 16; ++q4) dst[q4] = make_uint4(pn, pn, pn, pn);
+        } else {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(prm.out) + orow * kHeadDim);
+          for (int q4 = 0; q4 < 32; ++q4) dst[q4] = make_float4(nan, nan, nan, nan);
+        }
+        prm.lse[orow] = -INFINITY;
+      }
+      TR_ADD(5);  // softmax warps: item epilogue
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&s.meta_empty[sl][p]));
+    }
+    (void)qc;
+  }
+  TR_FLUSH();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+
+cudaError_t launch_attention_fa3(const Dims& D, const __nv_bfloat16* Q, const __nv_bfloat16* K,
+                                const __nv_bfloat16* V, const int32_t* idx, const int32_t* counts,
+                                bool out_bf16, void* out, float* lse, unsigned long long* visits,
+                                int32_t* plan_error, int* sched, uint16_t* lists, cudaStream_t s) {
+  CUtensorMap tm_q, tm_k, tm_v, tm_o;
+  if (!make_tmap_rows128(&tm_q, Q, D.L, (uint64_t)D.Z * D.Hq) ||
+      !make_tmap_rows128(&tm_k, K, D.L, (uint64_t)D.Z * D.Hkv) ||
+      !make_tmap_rows128(&tm_v, V, D.L, (uint64_t)D.Z * D.Hkv) ||
+      !make_tmap_rows128(&tm_o, out_bf16 ? out : Q, D.L, (uint64_t)D.Z * D.Hq))
+    return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(sched, 0, sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int num_items = D.Z * D.Hq * D.Mr;
+  const int grid = num_items < sms ? num_items : sms;
+  // K/V bytes of one KV group = 2 tensors x L x d x 2 B; keep gs groups' worth <= 64 MiB
+  // (measured: 32K prefers all 4 Qwen3 groups interleaved, 128K/256K one group at a time).
+  // FPB_FA_GS overrides (measurement switch).
+  static const int gs_env = [] {
+    const char* e = std::getenv("FPB_FA_GS");
+    return e ? std::atoi(e) : 0;
+  }();
+  int gs = gs_env;
+  if (gs <= 0) {
+    const double group_bytes = 2.0 * D.L * D.d * 2.0;
+    gs = (int)((64.0 * 1024 * 1024) / group_bytes);
+  }
+  gs = gs < 1 ? 1 : (gs > D.Hkv ? D.Hkv : gs);
+  while (D.Hkv % gs) --gs;
+  FaParams prm{D, idx, counts, out, lse, visits, plan_error, sched, lists, num_items,
+               out_bf16 ? 1 : 0, gs};
+  const size_t smem = sizeof(FaSmem) + 1024;
+  e = cudaFuncSetAttribute(fa3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fa3_kernel<<<grid, kThreads, smem, s>>>(tm_q, tm_k, tm_v, tm_o, prm);
+  return cudaGetLastError();
+}
+
+}  // namespace fpb
+

@@ -34,9 +34,6 @@ constexpr int kThreads = 384;
 constexpr int kTile = kBlock * kHeadDim * 2;  // 32 KiB bf16 tile
 constexpr int kRing = 5;                      // shared K/V tile ring
 constexpr float kRescaleThreshold = 8.0f;     // lazy O rescale (log2 units)
-#ifndef FPB_POLY_MASK
-#define FPB_POLY_MASK 0  // pairs p with (p & 3) in this bit mask use exp2_poly2 (FMA pipe)
-#endif
 
 struct FaParams {
   Dims D;
@@ -466,14 +463,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (full) {
 #pragma unroll
             for (int c = half * 64; c < half * 64 + 64; c += 2) {
-              float x0, x1, p0, p1;
+              // MUFU ex2 for every element: FMA-pipe emulation measured slower on B200
+              // (profiles/r1_fa_trace.txt)
+              float x0, x1;
               ffma2(x0, x1, __uint_as_float(v[c]), __uint_as_float(v[c + 1]), sc, sc, neg_m, neg_m);
-              if ((FPB_POLY_MASK >> ((c >> 1) & 3)) & 1) {
-                exp2_poly2(x0, x1, p0, p1);
-              } else {
-                p0 = ex2_approx(x0);
-                p1 = ex2_approx(x1);
-              }
+              const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
               const int a = ((c >> 1) & 3) * 2;
               fadd2(bs[a], bs[a + 1], bs[a], bs[a + 1], p0, p1);
               v[c >> 1] = pack_bf16x2(p0, p1);

@@ -324,25 +324,6 @@ __device__ __forceinline__ void fadd2(float& dx, float& dy, float ax, float ay, 
       : "=f"(dx), "=f"(dy)
       : "f"(ax), "f"(ay), "f"(bx), "f"(by));
 }
-// 2^x for a pair on the FMA pipe (FA4-style MUFU offload): Cody-Waite split x = n + f,
-// f in [-1/2, 1/2], degree-3 minimax for 2^f (max rel. error 7.5e-5, below the bf16 rounding of P),
-// exponent inserted with an integer shift-add.  x is clamped at -125 so n never underflows.
-__device__ __forceinline__ void exp2_poly2(float x0, float x1, float& p0, float& p1) {
-  x0 = fmaxf(x0, -125.0f);
-  x1 = fmaxf(x1, -125.0f);
-  float t0, t1, r0, r1, f0, f1;
-  fadd2(t0, t1, x0, x1, 12582912.0f, 12582912.0f);    // 1.5 * 2^23: round-to-nearest integer
-  fadd2(r0, r1, t0, t1, -12582912.0f, -12582912.0f);
-  fadd2(f0, f1, x0, x1, -r0, -r1);
-  float q0, q1;
-  ffma2(q0, q1, f0, f1, 0.05517112836241722f, 0.05517112836241722f, 0.24261008203029633f,
-        0.24261008203029633f);
-  ffma2(q0, q1, q0, q1, f0, f1, 0.6932609677314758f, 0.6932609677314758f);
-  ffma2(q0, q1, q0, q1, f0, f1, 0.9999281167984009f, 0.9999281167984009f);
-  p0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
-  p1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
-}
-
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);

@@ -129,64 +129,97 @@ __global__ void fill_plan_kernel(Dims D, int32_t* __restrict__ idx) {
   }
 }
 
-// Two-pass plan-only discovery, second pass: one warp per owned (z, h, I) row of the packed
-// (local max, energy) triangle.  normalize_block_scores (discovery.hpp:131-143), the max-based
-// threshold with sink / window retention (selection.hpp:63-92) and compress_indices
-// (selection.hpp:176-192) in three sweeps over the row (L1/L2-resident after the first).
-__global__ void select_rows_kernel(Dims D, const float2* __restrict__ rows,
-                                   int32_t* __restrict__ idx, int32_t* __restrict__ counts,
-                                   int prefilled) {
-  const long wrow = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const long nrows = (long)D.Z * D.Hq * D.Mr;
-  if (wrow >= nrows) return;
-  const int lane = threadIdx.x & 31;
-  const int h = (int)(wrow % D.Hq);
-  const long t = wrow / D.Hq;
-  const int I = owned_row(D, (int)(t % D.Mr));
-  const int z = (int)(t / D.Mr);
-  const int N = D.M;
-  const float2* r = rows + ((size_t)z * D.Hq + h) * ((size_t)D.M * (D.M + 1) / 2) +
-                    (size_t)I * (I + 1) / 2;
-  float rmax = kNegSentinel;
-  for (int J = lane; J <= I; J += 32) rmax = fmaxf(rmax, r[J].x);
-  rmax = warp_max(rmax);
-  float total = 0.f, pmax = 0.f;
-  for (int J = lane; J <= I; J += 32) {
-    const float2 ms = r[J];
-    const float sp = __fmul_rn(ms.y, exp2f(__fsub_rn(ms.x, rmax)));
-    total += sp;
-    pmax = fmaxf(pmax, sp);
-  }
-  total = warp_sum(total);
-  pmax = warp_max(pmax);
-  const float inv = __fdiv_rn(1.0f, __fadd_rn(total, D.eps));
-  // max_J fl(S'_J inv) == fl(max_J S'_J * inv) (monotone rounding, inv > 0); max_val >= 0
-  const float thresh = __fmul_rn(D.alpha, __fmul_rn(pmax, inv));
+// Two-pass plan-only discovery, second pass.  One CTA per owned (z, I) plan row and one warp per
+// head: normalize_block_scores (discovery.hpp:131-143), the max-based threshold with sink /
+// window retention (selection.hpp:63-92) and compress_indices (selection.hpp:176-192) in three
+// sweeps over the head's row of the packed (local max, energy) triangle.  The plan is head-last
+// (Z x M x N x H, selection.hpp:14-21), so the CTA assembles the N x Hc slab of a chunk of Hc
+// heads in shared memory (fill value N included) and writes it with coalesced stores; Hc is a
+// power of two and the slab is XOR-swizzled so both the per-head compaction writes (consecutive
+// slots) and the row-major copy-out are bank-conflict free.
+__global__ void __launch_bounds__(1024, 2) select_rows_kernel(Dims D, const float2* __restrict__ rows,
+                                                           int32_t* __restrict__ idx,
+                                                           int32_t* __restrict__ counts, int hc_log2) {
+  extern __shared__ int32_t slab[];
+  const int Hc = 1 << hc_log2;
+  const int N = D.M, H = D.Hq;
+  const int z = blockIdx.x / D.Mr;
+  const int I = owned_row(D, blockIdx.x % D.Mr);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t plan_row = ((size_t)z * D.M + I) * (size_t)N;
-  int base = 0;
-  for (int J0 = 0; J0 <= I; J0 += 32) {
-    const int J = J0 + lane;
-    bool act = false;
-    if (J <= I) {
-      const float2 ms = r[J];
-      const float sc = __fmul_rn(__fmul_rn(ms.y, exp2f(__fsub_rn(ms.x, rmax))), inv);
-      act = sc >= thresh || J < D.sink_blocks || (I - J) < D.window_blocks;
+  auto at = [&](int slot, int hc) { return slot * Hc + (hc ^ (slot & (Hc - 1))); };
+  for (int h0 = 0; h0 < H; h0 += Hc) {
+    const int Hv = min(Hc, H - h0);
+    for (int e = threadIdx.x; e < N * Hc; e += blockDim.x) slab[e] = N;
+    __syncthreads();
+    if (w < Hv) {
+      const int h = h0 + w;
+      const float2* r = rows + ((size_t)z * H + h) * ((size_t)D.M * (D.M + 1) / 2) +
+                        (size_t)I * (I + 1) / 2;
+      float rmax = kNegSentinel;
+      for (int J = lane; J <= I; J += 32) rmax = fmaxf(rmax, r[J].x);
+      rmax = warp_max(rmax);
+      float total = 0.f, pmax = 0.f;
+      for (int J = lane; J <= I; J += 32) {
+        const float2 ms = r[J];
+        const float sp = __fmul_rn(ms.y, exp2f(__fsub_rn(ms.x, rmax)));
+        total += sp;
+        pmax = fmaxf(pmax, sp);
+      }
+      total = warp_sum(total);
+      pmax = warp_max(pmax);
+      const float inv = __fdiv_rn(1.0f, __fadd_rn(total, D.eps));
+      // max_J fl(S'_J inv) == fl(max_J S'_J * inv) (monotone rounding, inv > 0); max_val >= 0
+      const float thresh = __fmul_rn(D.alpha, __fmul_rn(pmax, inv));
+      int base = 0;
+      for (int J0 = 0; J0 <= I; J0 += 32) {
+        const int J = J0 + lane;
+        bool act = false;
+        if (J <= I) {
+          const float2 ms = r[J];
+          const float sc = __fmul_rn(__fmul_rn(ms.y, exp2f(__fsub_rn(ms.x, rmax))), inv);
+          act = sc >= thresh || J < D.sink_blocks || (I - J) < D.window_blocks;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, act);
+        if (act) slab[at(base + __popc(bal & ((1u << lane) - 1u)), w)] = J;
+        base += __popc(bal);
+      }
+      if (lane == 0) counts[((size_t)z * D.M + I) * H + h] = base;
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, act);
-    if (act) idx[(plan_row + base + __popc(bal & ((1u << lane) - 1u))) * D.Hq + h] = J;
-    base += __popc(bal);
+    __syncthreads();
+    int32_t* dst = idx + plan_row * H + h0;
+    if (Hv == H && (H & 3) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+      // the whole (z, I) row is one contiguous N x H run
+      int4* d4 = reinterpret_cast<int4*>(dst);
+      for (int e = threadIdx.x; e < N * H / 4; e += blockDim.x) {
+        const int k = e * 4, slot = k / Hc, hc = k % Hc;
+        d4[e] = make_int4(slab[at(slot, hc)], slab[at(slot, hc + 1)], slab[at(slot, hc + 2)],
+                          slab[at(slot, hc + 3)]);
+      }
+    } else {
+      for (int e = threadIdx.x; e < N * Hv; e += blockDim.x) {
+        const int slot = e / Hv, hc = e % Hv;
+        dst[(size_t)slot * H + hc] = slab[at(slot, hc)];
+      }
+    }
+    __syncthreads();
   }
-  if (!prefilled)
-    for (int slot = base + lane; slot < N; slot += 32) idx[(plan_row + slot) * D.Hq + h] = N;
-  if (lane == 0) counts[((size_t)z * D.M + I) * D.Hq + h] = base;
 }
 
 cudaError_t launch_select_rows(const Dims& D, const float2* rows, int32_t* idx, int32_t* counts,
                                bool prefilled, cudaStream_t s) {
-  const long nrows = (long)D.Z * D.Hq * D.Mr;
-  if (nrows == 0) return cudaSuccess;
-  select_rows_kernel<<<(unsigned)((nrows + 7) / 8), 256, 0, s>>>(D, rows, idx, counts,
-                                                                  prefilled ? 1 : 0);
+  (void)prefilled;  // the slab carries the fill value; every slot of an owned row is written
+  const long nrows = (long)D.Z * D.Mr;
+  if (nrows == 0 || D.Hq == 0) return cudaSuccess;
+  int hc_log2 = 0;
+  while (hc_log2 < 5 && (2 << hc_log2) <= D.Hq) ++hc_log2;  // largest power of two <= min(H, 32)
+  while (hc_log2 > 0 && (size_t)D.M * (1u << hc_log2) * 4 > 96 * 1024) --hc_log2;
+  const size_t smem = (size_t)D.M * (1u << hc_log2) * 4;
+  if (smem > 96 * 1024) return cudaErrorInvalidValue;  // M > 24K blocks: not a two-pass size
+  cudaError_t e = cudaFuncSetAttribute(select_rows_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  if (e != cudaSuccess) return e;
+  select_rows_kernel<<<(unsigned)nrows, 32 << hc_log2, smem, s>>>(D, rows, idx, counts, hc_log2);
   return cudaGetLastError();
 }
 

@@ -108,6 +108,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id(), lane = lane_id();
   DT_DECL;
+#ifdef FPB_TRACE
+  const long long t_begin = clock64();
+#endif
 
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tm_q);
@@ -192,7 +195,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int gc = 0, dcw[2] = {0, 0};
       for (int t = 0;; ++t) {
         const int slot = t % kItemRing;
+        DT_T0();
         mbar_wait(smem_u32(&s.it_full[slot]), (t / kItemRing) & 1);
+        DT_ADD(19);  // MMA: waiting for the next item
         const int item = s.items[slot];
         mbar_arrive(smem_u32(&s.it_empty[slot]));
         if (item < 0) break;
@@ -444,6 +449,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       DT_ADD(4);  // epilogue: fill + counts
     }
   }
+#ifdef FPB_TRACE
+  if (threadIdx.x == 32) dt_acc[20] += (unsigned long long)(clock64() - t_begin);
+#endif
   DT_FLUSH();
   tc_fence_before();
   __syncthreads();

@@ -119,6 +119,38 @@ def test_fused_discover_select(fp, port, shape, alpha, with_maps):
     assert np.array_equal(gi.transpose(0, 1, 3, 2)[ok_rows], idx.transpose(0, 1, 3, 2)[ok_rows])
 
 
+@pytest.mark.parametrize("shape", [(1, 40, 8, 1000), (1, 64, 8, 700), (2, 6, 3, 1300),
+                                   (1, 1, 1, 2000), (1, 12, 4, 777)])
+def test_plan_only_two_pass_head_counts(fp, port, shape):
+    """Plan-only calls below 1024 key blocks run the two-pass path (discovery writes the (m, S)
+    triangle, select_rows assembles each head-last plan row slab).  Head counts that are not a
+    power of two, exceed one 32-head slab, or are 1 exercise the slab chunking and the scalar
+    copy-out; the plan must equal the reference outside the epsilon band (selection.hpp:63-92,
+    176-192)."""
+    Z, Hq, Hkv, L = shape
+    q, k, _ = composite_np(7 + L, Z, Hq, Hkv, L)
+    q, k = bf16_round(q), bf16_round(k)
+    tau = float(port.scale(128))
+    kk = np.repeat(k, Hq // Hkv, axis=1)
+    _, _, sc = port.discover(q, kk, 128, tau)
+    mask, _ = port.max_threshold_mask(sc, 128, 0.12, 256, 512)
+    idx, counts = port.compress_indices(mask)
+    plan = fp.discover_select(_cuda(q), _cuda(k), fp.PipelineConfig(alpha=0.12))[0]
+    gi, gc = _np(plan.indices), _np(plan.counts)
+    M = gc.shape[1]
+    zz, ii, ss, hh = np.meshgrid(np.arange(Z), np.arange(M), np.arange(M), np.arange(Hq),
+                                 indexing="ij")
+    live = ss < gc[:, :, None, :]
+    assert bool((gi[~live] == M).all())
+    gmask = np.zeros((Z, M, M + 1, Hq), bool)
+    gmask[zz[live], ii[live], gi[live], hh[live]] = True
+    bad, near, flipped = compare_masks(gmask[:, :, :M], mask, sc, 0.12)
+    assert bad == 0, (bad, near, flipped)
+    ok_rows = ~rows_with_near(sc, 0.12)
+    assert np.array_equal(gc[ok_rows], counts[ok_rows])
+    assert np.array_equal(gi.transpose(0, 1, 3, 2)[ok_rows], idx.transpose(0, 1, 3, 2)[ok_rows])
+
+
 def test_fused_discover_select_global_rows(fp, port, monkeypatch):
     """The long-sequence variant (per-key-block rows in a global scratch instead of shared memory,
     taken automatically beyond ~270K tokens) forced at a size the oracle finishes quickly."""

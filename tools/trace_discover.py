@@ -16,7 +16,8 @@ NAMES = {0: "epi wait accumulator", 1: "epi TMEM load", 2: "epi chunk max/exp2/s
          4: "epi fill (idx = N) + counts", 5: "epi wait item",
          8: "mma wait Q", 9: "mma wait accumulator free", 10: "mma wait kbar chunk",
          11: "mma issue", 12: "producer item ring full", 13: "producer Q buffer busy",
-         14: "producer kbar ring full", 15: "producer atomic"}
+         14: "producer kbar ring full", 15: "producer atomic", 19: "mma wait item",
+         20: "kernel cycles (CTA, warp 1 lane 0)"}
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 q, k, v = workload.composite(5, 1, 32, 4, L, device="cuda")
 cfg = fp.PipelineConfig()
@@ -35,8 +36,8 @@ chunks = 32 * sum(I // 128 + 1 for I in range(M))
 epi_warps = 148 * 8
 print(f"L={L}: items {items}, chunks {chunks}; per-SM totals in Kcycles (epilogue: per warp avg)")
 for i, n in NAMES.items():
-    if i < 8 or i >= 16:
+    if i < 8 or 16 <= i <= 18:
         per_sm = buf[i] / epi_warps / 1e3  # average per epilogue warp
     else:
         per_sm = buf[i] / 148 / 1e3
-    print(f"{n:40s} {per_sm:10.1f} Kcyc per {'epilogue warp' if (i < 8 or i >= 16) else 'SM'}")
+    print(f"{n:40s} {per_sm:10.1f} Kcyc per {'epilogue warp' if (i < 8 or 16 <= i <= 18) else 'SM'}")

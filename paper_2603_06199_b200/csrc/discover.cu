@@ -38,6 +38,18 @@ constexpr int kTile = kBlock * kHeadDim * 2;  // one bf16 128x128 operand tile: 
 constexpr int kStages = 2;                    // k̄ chunk ring (hi + lo per stage)
 constexpr int kItemRing = 4;
 constexpr uint32_t kEpiBar = 1;               // named barriers 1, 2: the two epilogue warpgroups
+// Control roles sit on the SM sub-partitions whose epilogue warps are least loaded: epilogue warp
+// w4 + i serves key blocks J = 32i..32i+31 of a chunk, and short causal chunks leave the high
+// quarters idle, so the single MMA-issuing thread (whose serial bookkeeping competes for issue
+// slots with the epilogue warps of its sub-partition) runs on warp 3.
+#ifndef FPB_DISC_MMA_WARP
+#define FPB_DISC_MMA_WARP 3
+#endif
+#ifndef FPB_DISC_PRODUCER_WARP
+#define FPB_DISC_PRODUCER_WARP 2
+#endif
+constexpr uint32_t kMmaWarp = FPB_DISC_MMA_WARP;
+constexpr uint32_t kProducerWarp = FPB_DISC_PRODUCER_WARP;
 
 struct DiscParams {
   Dims D;
@@ -58,6 +70,7 @@ struct DiscSmem {
   uint64_t d_full[4], d_empty[4];  // TMEM accumulators: 2 per epilogue warpgroup
   uint64_t it_full[kItemRing], it_empty[kItemRing];
   int items[kItemRing];
+  int nch[kItemRing];  // k̄ chunks of the item (I / 128 + 1), decoded once by the producer
   uint32_t tmem_base;
   float red[2][3][4];
   // followed by float m_s[M], S_s[M] per epilogue warpgroup, then int counts[ceil(M/128)][4]
@@ -139,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = s.tmem_base;
 
-  if (warp == 0) {
+  if (warp == kProducerWarp) {
     // ===================== scheduler + TMA producer
     if (elect_one()) {
       int gc = 0;  // global chunk counter (same sequence as the MMA issuer)
@@ -151,6 +164,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         int item = atomicAdd(prm.sched, 1);
         DT_ADD(15);  // producer: work-counter atomic
         if (item >= prm.num_items) item = -1;
+        int z = 0, h = 0, I = 0;
+        if (item >= 0) {
+          decode_item(D, item, z, h, I);
+          s.nch[slot] = I / kBlock + 1;
+        }
         s.items[slot] = item;
         mbar_arrive(smem_u32(&s.it_full[slot]));
         if (item < 0) {  // the other epilogue warpgroup needs its own end marker
@@ -160,8 +178,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(smem_u32(&s.it_full[slot2]));
           break;
         }
-        int z, h, I;
-        decode_item(D, item, z, h, I);
         const int zkv = z * D.Hkv + h / D.group;
         const int qb = t % kQBuf;
         DT_T0();
@@ -188,30 +204,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (one thread)
     if (elect_one()) {
       constexpr uint32_t idesc = idesc_bf16_f32(128, 128, false, false);
-      int gc = 0, dcw[2] = {0, 0};
+      int gc = 0, dc0 = 0, dc1 = 0;  // chunks issued in total / per epilogue warpgroup
       for (int t = 0;; ++t) {
         const int slot = t % kItemRing;
         DT_T0();
         mbar_wait(smem_u32(&s.it_full[slot]), (t / kItemRing) & 1);
         DT_ADD(19);  // MMA: waiting for the next item
         const int item = s.items[slot];
+        const int nchunks = s.nch[slot];
         mbar_arrive(smem_u32(&s.it_empty[slot]));
         if (item < 0) break;
-        int z, h, I;
-        decode_item(D, item, z, h, I);
         const int qb = t % kQBuf, wg = t & 1;
-        DT_T0();
+        DT_ADD(21);  // MMA: item decode
         mbar_wait(smem_u32(&s.q_full[qb]), (t / kQBuf) & 1);
         DT_ADD(8);  // MMA: waiting for Q
-        const int nchunks = I / kBlock + 1;
-        for (int c = 0; c < nchunks; ++c, ++gc, ++dcw[wg]) {
-          const int dc = dcw[wg];
+        for (int c = 0; c < nchunks; ++c, ++gc) {
+          const int dc = wg ? dc1++ : dc0++;
           const int st = gc % kStages, buf = wg * 2 + (dc & 1);
-          DT_T0();
+          DT_ADD(22);  // MMA: loop overhead between chunks
           if (dc >= 2) mbar_wait(smem_u32(&s.d_empty[buf]), ((dc >> 1) - 1) & 1);
           DT_ADD(9);  // MMA: waiting for the accumulator (epilogue behind)
           mbar_wait(smem_u32(&s.kb_full[st]), (gc / kStages) & 1);
@@ -450,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 #ifdef FPB_TRACE
-  if (threadIdx.x == 32) dt_acc[20] += (unsigned long long)(clock64() - t_begin);
+  if (threadIdx.x == kMmaWarp * 32) dt_acc[20] += (unsigned long long)(clock64() - t_begin);
 #endif
   DT_FLUSH();
   tc_fence_before();

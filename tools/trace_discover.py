@@ -16,8 +16,8 @@ NAMES = {0: "epi wait accumulator", 1: "epi TMEM load", 2: "epi chunk max/exp2/s
          4: "epi fill (idx = N) + counts", 5: "epi wait item",
          8: "mma wait Q", 9: "mma wait accumulator free", 10: "mma wait kbar chunk",
          11: "mma issue", 12: "producer item ring full", 13: "producer Q buffer busy",
-         14: "producer kbar ring full", 15: "producer atomic", 19: "mma wait item",
-         20: "kernel cycles (CTA, warp 1 lane 0)"}
+         14: "producer kbar ring full", 15: "producer atomic", 19: "mma wait item", 21: "mma item decode", 22: "mma chunk loop overhead",
+         20: "kernel cycles (CTA, MMA warp lane 0)"}
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 q, k, v = workload.composite(5, 1, 32, 4, L, device="cuda")
 cfg = fp.PipelineConfig()

@@ -16,9 +16,10 @@
 // Naively rounding k̄ to bf16 flips mask bits (SURVEY §7 hard part 1).
 //
 // Warp roles (384 threads, persistent):
-//   w0  scheduler + TMA producer: item ring, Q tiles (double-buffered), k̄ chunk ring
-//   w1  MMA issuer (single thread); TMEM accumulators double-buffered per epilogue warpgroup
-//   w2  TMEM allocator (512 cols);  w3 idle
+//   w2  TMEM allocator (512 cols), then scheduler + TMA producer: item ring (with each item's
+//       chunk count), Q tiles (double-buffered), k̄ chunk ring
+//   w3  MMA issuer (single thread); TMEM accumulators double-buffered per epilogue warpgroup
+//   w0, w1 idle (the control roles sit on the sub-partitions with the lightest epilogue load)
 //   w4..w7, w8..w11  two epilogue warpgroups, items alternating: TMEM -> (m, S) per pair, then
 //          row normalisation, threshold and compaction for the item while the MMA warp and the
 //          other warpgroup already work on the next ones.

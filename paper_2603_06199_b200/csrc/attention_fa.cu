@@ -113,6 +113,7 @@ struct SlotState {
   int nblk = 0;
   int item = 0;
   int qc = 0;     // items with nblk > 0 (Q loads / O lifetimes)
+  int zkv = 0;    // K/V plane of the current item (producer)
   int bc = 0;     // blocks processed (P / S / O barrier phases)
   bool active = true;
 };
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           int z, h, qi;
           decode(D, prm.gs, S.item, z, h, qi);
+          S.zkv = z * D.Hkv + h / D.group;
           {
             TR_T0();
             if (S.qc >= 1) mbar_wait(smem_u32(&s.q_empty[sl]), (S.qc - 1) & 1);
@@ -301,9 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++S.qc;
         }
         // ---- one unit: V(j-1) then K(j), matching the MMA issue order PV(j-1), QK(j)
-        int z, h, qi;
-        decode(D, prm.gs, S.item, z, h, qi);
-        const int zkv = z * D.Hkv + h / D.group;
+        const int zkv = S.zkv;
         const uint16_t* lst = list_of(sl, p);
         if (S.j >= 1) push(&tm_v, (dense ? S.j - 1 : (int)lst[S.j - 1]) * kBlock, zkv);
         if (S.j < S.nblk) push(&tm_k, (dense ? S.j : (int)lst[S.j]) * kBlock, zkv);

@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = s.tmem_base;
   // 384 threads x 168 regs at launch; hand the control warpgroup's share to the softmax WGs
+  // (128 x 72 + 256 x 216 = 64512 = the launch allocation: any more and setmaxnreg.inc blocks)
   if (warp < 4) {
   setmaxnreg_dec<72>();
   if (warp == 3) {
@@ -353,7 +354,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           TR_T0();
           mbar_wait(smem_u32(&s.kv_full[r]), (kvc / kRing) & 1);
           TR_ADD(8);  // MMA: waiting for V
-          const uint32_t vb = smem_u32(s.ring[r]);
+          // SW128 descriptors are linear in the address field (addr >> 4, 14 bits; SMEM < 256 KiB),
+          // so every K step is the tile's base descriptor plus a constant
+          const uint64_t vdesc = sdesc_sw128(smem_u32(s.ring[r]), kTile / 2, 1024);
           // keys 0..63 as soon as the first half of P is in TMEM, keys 64..127 after the rest
           for (int half = 0; half < 2; ++half) {
             mbar_wait(smem_u32(half ? &s.p_full[sl] : &s.p_half[sl]), (S.bc - 1) & 1);
@@ -363,8 +366,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int k4 = 0; k4 < 4; ++k4) {
                 const int ks = half * 4 + k4;
-                mma_bf16_ts(o_tmem, s_tmem + ks * 8, sdesc_sw128(vb + ks * 2048, kTile / 2, 1024),
-                            idesc_pv, (m > 0 || ks > 0) ? 1u : 0u);
+                mma_bf16_ts(o_tmem, s_tmem + ks * 8, vdesc + (uint64_t)(ks * 2048 >> 4), idesc_pv,
+                            (m > 0 || ks > 0) ? 1u : 0u);
               }
             }
             __syncwarp();
@@ -384,12 +387,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           TR_ADD(11);  // MMA: waiting for K
           if (leader) {
-            const uint32_t qb = smem_u32(s.q[sl]), kb = smem_u32(s.ring[r]);
+            const uint64_t qdesc = sdesc_sw128(smem_u32(s.q[sl]), 16, 1024);
+            const uint64_t kdesc = sdesc_sw128(smem_u32(s.ring[r]), 16, 1024);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
-              const uint32_t off = (ks >> 2) * (kTile / 2) + (ks & 3) * 32;
-              mma_bf16_ss(s_tmem, sdesc_sw128(qb + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024),
-                          idesc_qk, ks > 0 ? 1u : 0u);
+              const uint64_t off = ((ks >> 2) * (kTile / 2) + (ks & 3) * 32) >> 4;
+              mma_bf16_ss(s_tmem, qdesc + off, kdesc + off, idesc_qk, ks > 0 ? 1u : 0u);
             }
             mma_commit(smem_u32(&s.kv_empty[r]));
             mma_commit(smem_u32(&s.s_full[sl]));

@@ -233,18 +233,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           DT_ADD(10);  // MMA: waiting for the k̄ chunk
           tc_fence_after();
           const uint32_t d_tmem = tmem + buf * 128;
+          // SW128 descriptors are linear in the address field: base + constant per K step
+          const uint64_t a_hi = sdesc_sw128(smem_u32(s.kb[st][0]), 16, 1024);
+          const uint64_t a_lo = sdesc_sw128(smem_u32(s.kb[st][1]), 16, 1024);
+          const uint64_t b_q0 = sdesc_sw128(smem_u32(s.q[qb][0]), 16, 1024);
+          const uint64_t b_q1 = sdesc_sw128(smem_u32(s.q[qb][NQ - 1]), 16, 1024);
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {
-            const uint32_t off = (ks >> 2) * (kTile / 2) + (ks & 3) * 32;
-            const uint64_t a_hi = sdesc_sw128(smem_u32(s.kb[st][0]) + off, 16, 1024);
-            const uint64_t a_lo = sdesc_sw128(smem_u32(s.kb[st][1]) + off, 16, 1024);
-            const uint64_t b_q0 = sdesc_sw128(smem_u32(s.q[qb][0]) + off, 16, 1024);
-            mma_bf16_ss(d_tmem, a_hi, b_q0, idesc, ks > 0);
-            mma_bf16_ss(d_tmem, a_lo, b_q0, idesc, 1);
-            if constexpr (NQ == 2) {
-              const uint64_t b_q1 = sdesc_sw128(smem_u32(s.q[qb][NQ - 1]) + off, 16, 1024);
-              mma_bf16_ss(d_tmem, a_hi, b_q1, idesc, 1);
-            }
+            const uint64_t off = ((ks >> 2) * (kTile / 2) + (ks & 3) * 32) >> 4;
+            mma_bf16_ss(d_tmem, a_hi + off, b_q0 + off, idesc, ks > 0);
+            mma_bf16_ss(d_tmem, a_lo + off, b_q0 + off, idesc, 1);
+            if constexpr (NQ == 2) mma_bf16_ss(d_tmem, a_hi + off, b_q1 + off, idesc, 1);
           }
           mma_commit(smem_u32(&s.kb_empty[st]));
           mma_commit(smem_u32(&s.d_full[buf]));

@@ -10,6 +10,7 @@ over ranks (no data-path collective; the O/LSE all-gather bytes per rank are lis
 the pool gives one GPU per box).
 
 usage: python tools/lsweep.py [--Ls 4096,...] [--out profiles/r1_lsweep.jsonl]
+       python tools/lsweep.py --markdown profiles/r1_lsweep.jsonl > profiles/r1_lsweep.md
 """
 from __future__ import annotations
 
@@ -67,7 +68,58 @@ def stage(q, k, v, cfg, grid, tau, reps, rows=None):
     return t_disc, t_attn, fl, visits
 
 
+def _kl(L):
+    return f"{L // 1024}K"
+
+
+def markdown(path):
+    """Render a sweep .jsonl as the tables in profiles/r1_lsweep.md."""
+    recs = [json.loads(x) for x in open(path) if x.strip()]
+    _, tc = peaks()
+    one = [r for r in recs if r["G"] == 1]
+    print("# Sparse-prefill latency vs sequence length — Qwen3-30B-A3B layer (32 Q / 4 KV heads, "
+          f"d 128), bf16, alpha {one[0]['alpha'] if one else 0.12}\n")
+    print("`tools/lsweep.py` on one B200: each stage replayed from a CUDA graph (`PrefillRunner`), "
+          "CUDA events, median of 3-5; inputs resident in HBM; synthetic vertical+slash composite, "
+          "seed 5.")
+    print("Attention fraction = plan FLOPs (4dB^2 per off-diagonal visit, 4dB(B+1)/2 per diagonal "
+          f"visit) / kernel time / {tc} TFLOP/s")
+    print("(MEASURED_PEAKS.json sustained bf16). Discovery bytes = Q + K read + idx (M x N) + counts "
+          "written (SURVEY §8d).\n")
+    print("| L | density | pool ms | discover+select ms | sparse attn ms | step ms | dense K5 ms | "
+          "speedup vs dense | eff. TFLOP/s (dense-equiv) | attn alg. TFLOP/s | attn frac | "
+          "discovery GB/s | disc frac of HBM |")
+    print("|" + "---|" * 13)
+    for r in one:
+        dense = f"{r['dense_ms']:.2f}" if "dense_ms" in r else "-"
+        sp = f"{r['speedup_vs_dense']:.2f}" if "speedup_vs_dense" in r else "-"
+        print(f"| {_kl(r['L'])} | {r['density']:.3f} | {r['pool_ms']:.3f} | "
+              f"{r['discover_select_ms']:.3f} | {r['attention_ms']:.3f} | {r['step_ms']:.3f} | "
+              f"{dense} | {sp} | {r['eff_tflops']:.0f} | {r['attn_alg_tflops']:.0f} | "
+              f"{r['attn_frac']:.3f} | {r['disc_gbps']:.0f} | {r['disc_frac']:.3f} |")
+    print("\n## 2 / 4 / 8 GPUs: every rank's share timed alone on this GPU (the pool gives one GPU "
+          "per box)\n")
+    print("Step = max over ranks (no data-path collective). `kv_group`: the north_star partition "
+          "(rank owns KV heads; Qwen3 at 8 ranks splits each group's 8 Q heads 4+4).")
+    print("`rows`: rank r owns query blocks r, r+G, ... of every head (`fpb_*_rows`), K/V "
+          "replicated. The O+LSE all-gather after the kernels is not timed (bytes listed; ~2 ms at "
+          "256K/8 ranks at ~900 GB/s).\n")
+    print("| L | G | partition | step ms (max over ranks) | per-rank step ms | job eff. TFLOP/s | "
+          "all-gather bytes per rank |")
+    print("|" + "---|" * 7)
+    for r in recs:
+        if r["G"] == 1:
+            continue
+        ranks = ", ".join(f"{x:.2f}" for x in r["rank_step_ms"])
+        print(f"| {_kl(r['L'])} | {r['G']} | {r['partition']} | "
+              f"{r['step_ms_max_over_ranks']:.3f} | {ranks} | {r['eff_tflops_job']:.0f} | "
+              f"{r['gather_bytes_per_rank'] / 2**20:.0f} MiB |")
+
+
 def main():
+    if len(sys.argv) == 3 and sys.argv[1] == "--markdown":
+        markdown(sys.argv[2])
+        return
     ap = argparse.ArgumentParser()
     ap.add_argument("--Ls", default="4096,8192,16384,32768,65536,131072,262144")
     ap.add_argument("--alpha", type=float, default=0.12)

@@ -33,6 +33,9 @@ namespace {
 constexpr int kThreads = 384;
 constexpr int kTile = kBlock * kHeadDim * 2;  // 32 KiB bf16 tile
 constexpr int kRing = 5;                      // shared K/V tile ring
+#ifndef FPB_SCHED_SLEEP
+#define FPB_SCHED_SLEEP 256  // ns; measured: 128K -5.7%, 32K / 256K neutral (r1_ab_fa_sched_sleep)
+#endif
 constexpr float kRescaleThreshold = 8.0f;     // lazy O rescale (log2 units)
 
 struct FaParams {
@@ -177,7 +180,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int p = t[sl] & 1;
         if (t[sl] >= 2) {
           const bool ready = mbar_try_wait(smem_u32(&s.meta_empty[sl][p]), ((t[sl] >> 1) - 1) & 1);
-          if (!__shfl_sync(0xffffffffu, ready, 0)) continue;
+          if (!__shfl_sync(0xffffffffu, ready, 0)) {
+#if FPB_SCHED_SLEEP > 0
+            __nanosleep(FPB_SCHED_SLEEP);  // both slots run ahead: yield the issue slots
+#endif
+            continue;
+          }
         }
         __syncwarp();
         int item = 0;

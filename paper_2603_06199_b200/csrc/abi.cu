@@ -908,11 +908,27 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
   if (const char* e = getenv("FPB_E2E_CHUNKS")) min_chunks = atoi(e);
   int cq = group;
   while (cq % 2 == 0 && (int64_t)D.Z * D.Hq / cq < min_chunks) cq /= 2;
-  const int chunks_per_z = D.Hq / cq, nch = D.Z * chunks_per_z;
+  // chunk list (z, first Q head, heads); a chunk never spans KV groups.  The first and the last
+  // chunk are halved (when cq is even) to shorten the pipeline fill (H2D before the first
+  // kernel) and drain (last kernels + D2H after the last H2D).
+  struct Chunk { int z, q0, nh; };
+  std::vector<Chunk> ch;
+  for (int z = 0; z < D.Z; ++z)
+    for (int q0 = 0; q0 < D.Hq; q0 += cq) ch.push_back({z, q0, cq});
+  if (cq % 2 == 0 && ch.size() >= 4) {
+    const int h = cq / 2;
+    const Chunk f = ch.front(), l = ch.back();
+    ch.erase(ch.begin());
+    ch.insert(ch.begin(), {{f.z, f.q0, h}, {f.z, f.q0 + h, h}});
+    ch.pop_back();
+    ch.push_back({l.z, l.q0, h});
+    ch.push_back({l.z, l.q0 + h, h});
+  }
+  const int nch = (int)ch.size();
   const size_t es = dsz(dtype), eo = dsz(out_dtype), Ld = (size_t)D.L * D.d;
   const size_t qb = q_elems(D) * es, kb = kv_elems(D) * es, ob = q_elems(D) * eo,
                lb = (size_t)D.Z * D.Hq * D.L * 4;
-  fpb_problem sub = *p;
+  fpb_problem sub = *p;  // sized for the largest chunk (cq heads); sub.Hq is set per chunk
   sub.Z = 1;
   sub.Hq = cq;
   sub.Hkv = 1;
@@ -980,19 +996,20 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
   const uint8_t* hk = static_cast<const uint8_t*>(K);
   const uint8_t* hv = static_cast<const uint8_t*>(V);
   for (int i = 0; i < nch; ++i) {  // H2D: K/V of a group with its first chunk, then the Q slice
-    const int z = i / chunks_per_z, q0 = (i % chunks_per_z) * cq, kv = q0 / group;
+    const int z = ch[i].z, q0 = ch[i].q0, nh = ch[i].nh, kv = q0 / group;
     if (q0 % group == 0) {
       const size_t off = ((size_t)z * D.Hkv + kv) * Ld * es;
       FPB_CUDA(cudaMemcpyAsync(dk + off, hk + off, Ld * es, cudaMemcpyHostToDevice, s_in));
       FPB_CUDA(cudaMemcpyAsync(dv + off, hv + off, Ld * es, cudaMemcpyHostToDevice, s_in));
     }
     const size_t off = ((size_t)z * D.Hq + q0) * Ld * es;
-    FPB_CUDA(cudaMemcpyAsync(dq + off, hq + off, cq * Ld * es, cudaMemcpyHostToDevice, s_in));
+    FPB_CUDA(cudaMemcpyAsync(dq + off, hq + off, nh * Ld * es, cudaMemcpyHostToDevice, s_in));
     FPB_CUDA(cudaEventRecord(ev_in[i], s_in));
     if ((rc = tr_mark(tr_in, s_in))) return rc;
   }
   for (int i = 0; i < nch; ++i) {  // kernels of each chunk on alternating compute streams
-    const int z = i / chunks_per_z, q0 = (i % chunks_per_z) * cq, kv = q0 / group;
+    const int z = ch[i].z, q0 = ch[i].q0, kv = q0 / group;
+    sub.Hq = ch[i].nh;
     cudaStream_t cs = sc[i & 1];
     void* ws = wsc[i & 1];
     FPB_CUDA(cudaStreamWaitEvent(cs, ev_in[i], 0));
@@ -1012,21 +1029,21 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
   }
   uint8_t* ho = static_cast<uint8_t*>(out);
   for (int i = 0; i < nch; ++i) {  // D2H of each finished chunk
-    const int z = i / chunks_per_z, q0 = (i % chunks_per_z) * cq;
+    const int z = ch[i].z, q0 = ch[i].q0, nh = ch[i].nh;
     FPB_CUDA(cudaStreamWaitEvent(s_out, ev_done[i], 0));
     const size_t oo = ((size_t)z * D.Hq + q0) * Ld * eo;
-    FPB_CUDA(cudaMemcpyAsync(ho + oo, dout + oo, cq * Ld * eo, cudaMemcpyDeviceToHost, s_out));
+    FPB_CUDA(cudaMemcpyAsync(ho + oo, dout + oo, nh * Ld * eo, cudaMemcpyDeviceToHost, s_out));
     const size_t lo = ((size_t)z * D.Hq + q0) * D.L;
-    FPB_CUDA(cudaMemcpyAsync(lse + lo, dl + lo, (size_t)cq * D.L * 4, cudaMemcpyDeviceToHost,
+    FPB_CUDA(cudaMemcpyAsync(lse + lo, dl + lo, (size_t)nh * D.L * 4, cudaMemcpyDeviceToHost,
                              s_out));
     // plans are head-last: scatter the chunk's heads into the caller's Z x M x N x Hq layout
     if (idx)
       FPB_CUDA(cudaMemcpy2DAsync(idx + (size_t)z * D.M * D.M * D.Hq + q0, (size_t)D.Hq * 4, di[i],
-                                 (size_t)cq * 4, (size_t)cq * 4, (size_t)D.M * D.M,
+                                 (size_t)nh * 4, (size_t)nh * 4, (size_t)D.M * D.M,
                                  cudaMemcpyDeviceToHost, s_out));
     if (counts)
       FPB_CUDA(cudaMemcpy2DAsync(counts + (size_t)z * D.M * D.Hq + q0, (size_t)D.Hq * 4, dc[i],
-                                 (size_t)cq * 4, (size_t)cq * 4, (size_t)D.M,
+                                 (size_t)nh * 4, (size_t)nh * 4, (size_t)D.M,
                                  cudaMemcpyDeviceToHost, s_out));
     if ((rc = tr_mark(tr_out, s_out))) return rc;
   }

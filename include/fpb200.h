@@ -128,6 +128,22 @@ int fpb_block_sparse_attention_rows(const fpb_problem* p, int32_t row_begin, int
                                     fpb_dtype out_dtype, void* out, float* lse,
                                     unsigned long long* visits, int32_t* plan_error,
                                     void* workspace, size_t workspace_bytes, void* stream);
+/* Zigzag shard: the query blocks are cut into 2 * world contiguous chunks of
+ * ceil(M / (2 * world)) blocks and rank owns chunks `rank` and `2 * world - 1 - rank` -- equal
+ * causal work per rank like the interleaved shard above, but contiguous rows, so the concurrently
+ * processed rows of a rank share their K/V blocks in L2 as in the unsharded call.
+ * 0 <= rank < world; otherwise as the _rows entry points. */
+int fpb_discover_select_zigzag(const fpb_problem* p, int32_t rank, int32_t world,
+                               fpb_dtype dtype, const void* Q, const void* K, float* energy,
+                               float* local_max, float* score, uint8_t* mask, int32_t* idx,
+                               int32_t* counts, void* workspace, size_t workspace_bytes,
+                               void* stream);
+int fpb_block_sparse_attention_zigzag(const fpb_problem* p, int32_t rank, int32_t world,
+                                      fpb_dtype dtype, const void* Q, const void* K,
+                                      const void* V, const int32_t* idx, const int32_t* counts,
+                                      fpb_dtype out_dtype, void* out, float* lse,
+                                      unsigned long long* visits, int32_t* plan_error,
+                                      void* workspace, size_t workspace_bytes, void* stream);
 
 /* dense_attention (attention.hpp:135-174): the dense causal kernel, the speedup denominator. */
 int fpb_dense_attention(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,

@@ -21,6 +21,7 @@ EXPORTS = [
     "fpb_max_threshold_mask", "fpb_compress_indices", "fpb_discover_select", "fpb_visit_count",
     "fpb_block_sparse_attention", "fpb_dense_attention", "fpb_full_causal_plan",
     "fpb_discover_select_rows", "fpb_block_sparse_attention_rows",
+    "fpb_discover_select_zigzag", "fpb_block_sparse_attention_zigzag",
     "fpb_topk_select", "fpb_topp_select", "fpb_baseline_workspace_bytes",
     "fpb_discover_pool_both", "fpb_discover_exact",
     "fpb_host_pool_keys", "fpb_host_approx_block_scores", "fpb_host_normalize_block_scores",
@@ -73,6 +74,11 @@ def lib() -> C.CDLL:
             "fpb_block_sparse_attention_rows": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int, p, p,
                                                           p, p, p, C.c_int, p, p, p, p, p,
                                                           C.c_size_t, p]),
+            "fpb_discover_select_zigzag": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int, p, p, p,
+                                                     p, p, p, p, p, p, C.c_size_t, p]),
+            "fpb_block_sparse_attention_zigzag": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int, p,
+                                                            p, p, p, p, C.c_int, p, p, p, p, p,
+                                                            C.c_size_t, p]),
             "fpb_visit_count": (C.c_int, [P, p, p, p]),
             "fpb_block_sparse_attention": (C.c_int, [P, C.c_int, p, p, p, p, p, C.c_int, p, p, p,
                                                      p, p, C.c_size_t, p]),

@@ -443,13 +443,22 @@ def density(plan: SparseBlockPlan, grid: BlockGrid) -> float:
     return visit_count(plan) / (Z * H * (M * (M + 1) / 2.0))
 
 
+def _rows_args(rows):
+    """(entry-point suffix, a, b) of a row shard: (row_begin, row_step) for the interleaved shard
+    (fpb_*_rows), ("zigzag", rank, world) for the zigzag shard (fpb_*_zigzag)."""
+    if len(rows) == 3 and rows[0] == "zigzag":
+        return "zigzag", int(rows[1]), int(rows[2])
+    return "rows", int(rows[0]), int(rows[1])
+
+
 def discover_select(queries: torch.Tensor, keys: torch.Tensor, config: PipelineConfig,
                     want_score: bool = False, want_mask: bool = False,
                     want_energy: bool = False, rows: tuple[int, int] | None = None):
     """Fused discover -> max_threshold_mask -> compress_indices (one pass over Q).
 
     rows=(row_begin, row_step) restricts the work to query blocks row_begin + row_step * k
-    (fpb_discover_select_rows, the row-sharded multi-GPU partition); rows of other blocks in the
+    (fpb_discover_select_rows, the row-sharded multi-GPU partition); rows=("zigzag", rank, world)
+    to rank's two contiguous chunks (fpb_discover_select_zigzag); rows of other blocks in the
     returned tensors are left unwritten.
     Returns (SparseBlockPlan, BlockScoreMap | None, ActiveMask | None)."""
     config.validate()
@@ -472,10 +481,11 @@ def discover_select(queries: torch.Tensor, keys: torch.Tensor, config: PipelineC
                                               _ptr(mask), _ptr(idx), _ptr(counts), _ptr(ws), nws,
                                               _stream(queries)), "discover_select")
     else:
-        _raise(_abi.lib().fpb_discover_select_rows(
-            C.byref(p), int(rows[0]), int(rows[1]), _dtype_code(queries), _ptr(queries),
+        kind, a, b = _rows_args(rows)
+        _raise(getattr(_abi.lib(), f"fpb_discover_select_{kind}")(
+            C.byref(p), a, b, _dtype_code(queries), _ptr(queries),
             _ptr(keys), _ptr(en), _ptr(lm), _ptr(score), _ptr(mask), _ptr(idx), _ptr(counts),
-            _ptr(ws), nws, _stream(queries)), "discover_select_rows")
+            _ptr(ws), nws, _stream(queries)), f"discover_select_{kind}")
     smap = BlockScoreMap(en, lm, score) if want_score else None
     return SparseBlockPlan(idx, counts), smap, (ActiveMask(mask) if want_mask else None)
 
@@ -502,7 +512,8 @@ def block_sparse_attention(queries, keys, values, plan: SparseBlockPlan, grid: B
     """attention.hpp:38-132.  Raises PlanError for a block index outside [0, N).
 
     rows=(row_begin, row_step): only query blocks row_begin + row_step * k are computed
-    (fpb_block_sparse_attention_rows); output rows of other blocks are left unwritten."""
+    (fpb_block_sparse_attention_rows); rows=("zigzag", rank, world): rank's zigzag chunks
+    (fpb_block_sparse_attention_zigzag); output rows of other blocks are left unwritten."""
     _check_qkv(queries, keys, values)
     Z, Hq, L, d = queries.shape
     M = grid.num_query_blocks
@@ -524,11 +535,12 @@ def block_sparse_attention(queries, keys, values, plan: SparseBlockPlan, grid: B
             C.c_void_p(aux.data_ptr() + 8), _ptr(ws), nws, _stream(queries)),
             "block_sparse_attention")
     else:
-        _raise(_abi.lib().fpb_block_sparse_attention_rows(
-            C.byref(p), int(rows[0]), int(rows[1]), _dtype_code(queries), _ptr(queries),
+        kind, a, b = _rows_args(rows)
+        _raise(getattr(_abi.lib(), f"fpb_block_sparse_attention_{kind}")(
+            C.byref(p), a, b, _dtype_code(queries), _ptr(queries),
             _ptr(keys), _ptr(values), _ptr(idx), _ptr(counts), oc, _ptr(out), _ptr(lse),
             C.c_void_p(aux.data_ptr()), C.c_void_p(aux.data_ptr() + 8), _ptr(ws), nws,
-            _stream(queries)), "block_sparse_attention_rows")
+            _stream(queries)), f"block_sparse_attention_{kind}")
     visits, err = (int(x) for x in aux.tolist())
     if err:
         raise PlanError(f"plan row lists a block index outside [0, {M})")
@@ -615,7 +627,8 @@ class PrefillRunner:
     to raise PlanError like the reference).  capture() records each stage into a CUDA graph, so a
     step is two graph launches (the launch-bound inner loop without a tracing compiler).
 
-    rows=(row_begin, row_step) runs one rank's row shard (fpb_*_rows)."""
+    rows=(row_begin, row_step) runs one rank's row shard (fpb_*_rows), rows=("zigzag", rank, world)
+    its zigzag shard (fpb_*_zigzag)."""
 
     def __init__(self, queries, keys, values, config: PipelineConfig,
                  out_dtype: torch.dtype = torch.bfloat16, rows: tuple[int, int] | None = None):
@@ -652,10 +665,10 @@ class PrefillRunner:
                                          None, None, None, None, _ptr(self.idx),
                                          _ptr(self.counts), _ptr(self.ws), self.nws, s)
         else:
-            rc = lib.fpb_discover_select_rows(C.byref(self.p), self.rows[0], self.rows[1], self.dt,
-                                              _ptr(self.q), _ptr(self.k), None, None, None, None,
-                                              _ptr(self.idx), _ptr(self.counts), _ptr(self.ws),
-                                              self.nws, s)
+            kind, a, b = _rows_args(self.rows)
+            rc = getattr(lib, f"fpb_discover_select_{kind}")(
+                C.byref(self.p), a, b, self.dt, _ptr(self.q), _ptr(self.k), None, None, None, None,
+                _ptr(self.idx), _ptr(self.counts), _ptr(self.ws), self.nws, s)
         _raise(rc, "discover_select")
 
     def attend(self):
@@ -667,8 +680,9 @@ class PrefillRunner:
                 _ptr(self.counts), self.oc, _ptr(self.out), _ptr(self.lse), vis, err,
                 _ptr(self.ws), self.nws, s)
         else:
-            rc = lib.fpb_block_sparse_attention_rows(
-                C.byref(self.p), self.rows[0], self.rows[1], self.dt, _ptr(self.q), _ptr(self.k),
+            kind, a, b = _rows_args(self.rows)
+            rc = getattr(lib, f"fpb_block_sparse_attention_{kind}")(
+                C.byref(self.p), a, b, self.dt, _ptr(self.q), _ptr(self.k),
                 _ptr(self.v), _ptr(self.idx), _ptr(self.counts), self.oc, _ptr(self.out),
                 _ptr(self.lse), vis, err, _ptr(self.ws), self.nws, s)
         _raise(rc, "block_sparse_attention")

@@ -103,6 +103,7 @@ int resolve(const fpb_problem* p, Dims* D) {
   D->rb = 0;
   D->rs = 1;
   D->Mr = D->M;
+  D->zz = D->zh_end = D->zh_n = D->zl_end = 0;
   return FPB_OK;
 }
 
@@ -115,6 +116,24 @@ int restrict_rows(Dims* D, int32_t row_begin, int32_t row_step) {
   D->rb = row_begin;
   D->rs = row_step;
   D->Mr = row_begin < D->M ? (D->M - row_begin + row_step - 1) / row_step : 0;
+  return FPB_OK;
+}
+
+// Restrict a resolved problem to rank's zigzag shard of world: chunks `rank` and
+// `2 world - 1 - rank` of 2 world contiguous chunks of ceil(M / (2 world)) query blocks.
+int restrict_zigzag(Dims* D, int32_t rank, int32_t world) {
+  if (world < 1 || rank < 0 || rank >= world)
+    return fail(FPB_EVALIDATION, "zigzag shard needs 0 <= rank < world");
+  if (world > 1 && !(D->d == kHeadDim && D->B == kBlock))
+    return fail(FPB_EVALIDATION, "row sharding needs d = block_size = 128");
+  const int64_t c = (D->M + 2 * (int64_t)world - 1) / (2 * (int64_t)world);
+  const int64_t hi0 = (2 * (int64_t)world - 1 - rank) * c, lo0 = rank * c;
+  const int64_t hi1 = std::min<int64_t>(D->M, hi0 + c), lo1 = std::min<int64_t>(D->M, lo0 + c);
+  D->zz = 1;
+  D->zh_end = (int)hi1;
+  D->zh_n = (int)std::max<int64_t>(0, hi1 - hi0);
+  D->zl_end = (int)lo1;
+  D->Mr = D->zh_n + (int)std::max<int64_t>(0, lo1 - lo0);
   return FPB_OK;
 }
 
@@ -299,10 +318,13 @@ static int discover_select_rows(const fpb_problem* p, int32_t row_begin, int32_t
                                 fpb_dtype dtype, const void* Q, const void* K, float* energy,
                                 float* local_max, float* score, uint8_t* mask, int32_t* idx,
                                 int32_t* counts, void* workspace, size_t workspace_bytes,
-                                void* stream) {
+                                void* stream, bool zigzag = false) {
   Dims D;
   int rc = resolve(p, &D);
-  if (rc || (rc = check_dtype(dtype)) || (rc = restrict_rows(&D, row_begin, row_step))) return rc;
+  if (rc || (rc = check_dtype(dtype)) ||
+      (rc = zigzag ? restrict_zigzag(&D, row_begin, row_step)
+                   : restrict_rows(&D, row_begin, row_step)))
+    return rc;
   if (!Q || !K) return fail(FPB_EUSAGE, "null pointer");
   if ((idx == nullptr) != (counts == nullptr))
     return fail(FPB_EUSAGE, "idx and counts must be given together");
@@ -362,6 +384,15 @@ int fpb_discover_select_rows(const fpb_problem* p, int32_t row_begin, int32_t ro
                              void* stream) {
   return discover_select_rows(p, row_begin, row_step, dtype, Q, K, energy, local_max, score, mask,
                               idx, counts, workspace, workspace_bytes, stream);
+}
+
+int fpb_discover_select_zigzag(const fpb_problem* p, int32_t rank, int32_t world,
+                               fpb_dtype dtype, const void* Q, const void* K, float* energy,
+                               float* local_max, float* score, uint8_t* mask, int32_t* idx,
+                               int32_t* counts, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+  return discover_select_rows(p, rank, world, dtype, Q, K, energy, local_max, score, mask, idx,
+                              counts, workspace, workspace_bytes, stream, true);
 }
 
 int fpb_discover(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
@@ -490,11 +521,12 @@ static int attention_common(const fpb_problem* p, fpb_dtype dtype, const void* Q
                             fpb_dtype out_dtype, void* out, float* lse,
                             unsigned long long* visits, int32_t* plan_error, void* workspace,
                             size_t workspace_bytes, void* stream, int32_t row_begin = 0,
-                            int32_t row_step = 1) {
+                            int32_t row_step = 1, bool zigzag = false) {
   Dims D;
   int rc = resolve(p, &D);
   if (rc || (rc = check_dtype(dtype)) || (rc = check_dtype(out_dtype)) ||
-      (rc = restrict_rows(&D, row_begin, row_step)))
+      (rc = zigzag ? restrict_zigzag(&D, row_begin, row_step)
+                   : restrict_rows(&D, row_begin, row_step)))
     return rc;
   if (!Q || !K || !V || !out || !lse) return fail(FPB_EUSAGE, "null pointer");
   if ((rc = need_ws(workspace_bytes, ws_attention(D, dtype), workspace))) return rc;
@@ -553,6 +585,17 @@ int fpb_block_sparse_attention_rows(const fpb_problem* p, int32_t row_begin, int
   if (!idx || !counts) return fail(FPB_EUSAGE, "null plan");
   return attention_common(p, dtype, Q, K, V, idx, counts, out_dtype, out, lse, visits, plan_error,
                           workspace, workspace_bytes, stream, row_begin, row_step);
+}
+
+int fpb_block_sparse_attention_zigzag(const fpb_problem* p, int32_t rank, int32_t world,
+                                      fpb_dtype dtype, const void* Q, const void* K,
+                                      const void* V, const int32_t* idx, const int32_t* counts,
+                                      fpb_dtype out_dtype, void* out, float* lse,
+                                      unsigned long long* visits, int32_t* plan_error,
+                                      void* workspace, size_t workspace_bytes, void* stream) {
+  if (!idx || !counts) return fail(FPB_EUSAGE, "null plan");
+  return attention_common(p, dtype, Q, K, V, idx, counts, out_dtype, out, lse, visits, plan_error,
+                          workspace, workspace_bytes, stream, rank, world, true);
 }
 
 int fpb_dense_attention(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,

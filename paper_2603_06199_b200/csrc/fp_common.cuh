@@ -27,11 +27,16 @@ struct Dims {
   // selection.hpp:71-72, attention.hpp:59-60), so rs ranks with rb = rank split any density
   // profile evenly.
   int rb, rs, Mr;
+  // Zigzag shard (zz = 1): 2G contiguous chunks of ceil(M / 2G) query blocks; rank r owns chunk r
+  // and chunk 2G-1-r (equal causal work, contiguous rows for K/V locality in L2).  zh_end / zh_n:
+  // end and size of the high chunk, zl_end: end of the low chunk; Mr = both sizes.
+  int zz, zh_end, zh_n, zl_end;
 };
 using GenDims = Dims;
 
 // t-th owned query block, heaviest (longest causal row) first.
 __host__ __device__ __forceinline__ int owned_row(const Dims& D, int t) {
+  if (D.zz) return t < D.zh_n ? D.zh_end - 1 - t : D.zl_end - 1 - (t - D.zh_n);
   return D.rb + D.rs * (D.Mr - 1 - t);
 }
 

@@ -101,6 +101,51 @@ def row_shard(world: int, rank: int) -> tuple[int, int]:
     return rank, world
 
 
+def zigzag_shard(world: int, rank: int) -> tuple[str, int, int]:
+    """Rank's zigzag shard (fpb_*_zigzag): query blocks cut into 2 * world contiguous chunks of
+    ceil(M / (2 world)); rank owns chunks rank and 2 world - 1 - rank (equal causal work,
+    contiguous rows)."""
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    return ("zigzag", rank, world)
+
+
+def zigzag_blocks(M: int, world: int, rank: int) -> list[int]:
+    """The query blocks a zigzag shard owns (ascending); mirrors restrict_zigzag in csrc/abi.cu."""
+    c = -(-M // (2 * world))
+    lo = range(rank * c, min(M, (rank + 1) * c))
+    hi = range((2 * world - 1 - rank) * c, min(M, (2 * world - rank) * c))
+    return list(lo) + list(hi)
+
+
+def gather_zigzag(out: torch.Tensor, lse: torch.Tensor, block: int, group=None):
+    """All-gather a zigzag-sharded result (every rank holds full-size out / lse with only its two
+    chunks written); returns the assembled tensors."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    res = []
+    for x in (out, lse):
+        Z, H, L = x.shape[:3]
+        M = -(-L // block)
+        c = -(-M // (2 * world))
+        Lp = 2 * world * c * block
+        if Lp != L:
+            pad = torch.zeros((Z, H, Lp) + tuple(x.shape[3:]), dtype=x.dtype, device=x.device)
+            pad[:, :, :L] = x
+            x = pad
+        xc = x.view((Z, H, 2 * world, c * block) + tuple(x.shape[3:]))
+        mine = torch.stack((xc[:, :, rank], xc[:, :, 2 * world - 1 - rank]), dim=2).contiguous()
+        allr = torch.empty((world * Z,) + tuple(mine.shape[1:]), dtype=x.dtype, device=x.device)
+        dist.all_gather_into_tensor(allr, mine, group=group)
+        allr = allr.view((world,) + tuple(mine.shape))  # rank, Z, H, 2, cB, ...
+        chunks = [allr[r, :, :, 0] for r in range(world)] + \
+                 [allr[r, :, :, 1] for r in reversed(range(world))]
+        full = torch.stack(chunks, dim=2).reshape((Z, H, Lp) + tuple(x.shape[3:]))[:, :, :L]
+        res.append(full.contiguous())
+    return res[0], res[1]
+
+
 def _row_blocks(x: torch.Tensor, block: int, world: int):
     """Pad the L axis (dim 2) to a multiple of block * world and expose (.., M/world, world, B, ..)."""
     Z, H, L = x.shape[:3]

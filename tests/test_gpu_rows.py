@@ -42,6 +42,60 @@ def test_row_shards_equal_whole(fp, world, dtype):
     assert bool(seen.all())
 
 
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_zigzag_shards_equal_whole(fp, world):
+    """Zigzag shards (fpb_*_zigzag: chunks rank and 2G-1-rank of 2G contiguous chunks) produce
+    exactly the unsharded plan rows and output rows, and together cover every query block; world 8
+    at M = 24 leaves some ranks' high chunk partly or wholly beyond the last block."""
+    Z, Hq, Hkv, L = 2, 4, 2, 3000  # ragged last block, M = 24
+    q, k, v = fp.workload.composite(9, Z, Hq, Hkv, L, device="cuda")
+    cfg = fp.PipelineConfig(alpha=0.12)
+    grid = fp.make_block_grid(L, 128)
+    tau = 1 / math.sqrt(128)
+    M = grid.num_query_blocks
+    plan = fp.discover_select(q, k, cfg)[0]
+    whole = fp.block_sparse_attention(q, k, v, plan, grid, tau, out_dtype=torch.float32)
+    seen = torch.zeros(M, dtype=torch.int32)
+    for rank in range(world):
+        rows = fp.shard.zigzag_shard(world, rank)
+        own = fp.shard.zigzag_blocks(M, world, rank)
+        seen[own] += 1
+        pr = fp.discover_select(q, k, cfg, rows=rows)[0]
+        assert torch.equal(pr.counts[:, own], plan.counts[:, own])
+        for I in own:
+            assert torch.equal(pr.indices[:, I], plan.indices[:, I])
+        res = fp.block_sparse_attention(q, k, v, pr, grid, tau, out_dtype=torch.float32,
+                                        rows=rows)
+        for I in own:
+            sl = slice(I * 128, min(L, (I + 1) * 128))
+            assert torch.equal(res.out[:, :, sl], whole.out[:, :, sl])
+            assert torch.equal(res.lse[:, :, sl], whole.lse[:, :, sl])
+    assert bool((seen == 1).all())
+
+
+def test_zigzag_runner_and_validation(fp):
+    """PrefillRunner graphs on a zigzag shard reproduce the direct calls; rank outside
+    [0, world) is a ValidationError."""
+    Z, Hq, Hkv, L = 1, 4, 2, 2000
+    q, k, v = fp.workload.composite(4, Z, Hq, Hkv, L, device="cuda")
+    cfg = fp.PipelineConfig(alpha=0.1)
+    grid = fp.make_block_grid(L, 128)
+    M = grid.num_query_blocks
+    plan = fp.discover_select(q, k, cfg)[0]
+    ref = fp.block_sparse_attention(q, k, v, plan, grid, cfg.resolved_scale(128),
+                                    out_dtype=torch.bfloat16)
+    rows = fp.shard.zigzag_shard(3, 1)
+    r = fp.PrefillRunner(q, k, v, cfg, out_dtype=torch.bfloat16, rows=rows).capture()
+    r.replay_discover()
+    r.replay_attend()
+    r.check()
+    for I in fp.shard.zigzag_blocks(M, 3, 1):
+        sl = slice(I * 128, min(L, (I + 1) * 128))
+        assert torch.equal(r.out[:, :, sl], ref.out[:, :, sl])
+    with pytest.raises(fp.ValidationError):
+        fp.discover_select(q, k, cfg, rows=("zigzag", 3, 3))
+
+
 def test_row_shard_beyond_blocks_is_noop(fp):
     """A rank whose row_begin is past the last block owns nothing: both calls return without
     touching their outputs."""

@@ -5,6 +5,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -93,3 +94,49 @@ def test_row_shard_gather_ragged_three_ranks():
     ret = mgr.dict()
     mp.spawn(_rows_worker, args=(world, _free_port(), out, lse, ret), nprocs=world, join=True)
     assert np.array_equal(ret["out"], out.numpy()) and np.array_equal(ret["lse"], lse.numpy())
+
+
+def _zigzag_worker(rank, world, port, out, lse, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_06199_b200.shard import gather_zigzag, zigzag_blocks
+    L = out.shape[2]
+    own = torch.zeros(L, dtype=torch.bool)
+    for I in zigzag_blocks(-(-L // 128), world, rank):
+        own[I * 128:(I + 1) * 128] = True
+    # rows this rank does not own are garbage in its buffers (fpb_*_zigzag leaves them unwritten)
+    o = torch.where(own[None, None, :, None], out, torch.full_like(out, float("nan")))
+    l_ = torch.where(own[None, None, :], lse, torch.full_like(lse, -7.0))
+    go, gl = gather_zigzag(o, l_, 128)
+    if rank == 0:
+        ret["out"] = go.numpy()
+        ret["lse"] = gl.numpy()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,L", [(2, 1000), (3, 1300)])
+def test_zigzag_shard_gather(world, L):
+    """Zigzag partition (two contiguous chunks per rank): the all-gather reassembles the full
+    output, including a ragged last block and a chunk grid that does not divide M."""
+    g = torch.Generator().manual_seed(world)
+    Z, Hq, d = 2, 3, 128
+    out = torch.randn((Z, Hq, L, d), generator=g)
+    lse = torch.randn((Z, Hq, L), generator=g)
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_zigzag_worker, args=(world, _free_port(), out, lse, ret), nprocs=world, join=True)
+    assert np.array_equal(ret["out"], out.numpy()) and np.array_equal(ret["lse"], lse.numpy())
+
+
+@pytest.mark.parametrize("M", [1, 5, 16, 17, 100, 2048])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_zigzag_blocks_partition(M, world):
+    """Every query block is owned by exactly one rank; each rank owns at most two contiguous
+    chunks of ceil(M / 2 world) blocks."""
+    from paper_2603_06199_b200.shard import zigzag_blocks
+    owned = [zigzag_blocks(M, world, r) for r in range(world)]
+    assert sorted(b for o in owned for b in o) == list(range(M))
+    c = -(-M // (2 * world))
+    assert all(len(o) <= 2 * c for o in owned)

@@ -102,8 +102,9 @@ def markdown(path):
     print("Step = max over ranks (no data-path collective). `kv_group`: the north_star partition "
           "(rank owns KV heads; Qwen3 at 8 ranks splits each group's 8 Q heads 4+4).")
     print("`rows`: rank r owns query blocks r, r+G, ... of every head (`fpb_*_rows`), K/V "
-          "replicated. The O+LSE all-gather after the kernels is not timed (bytes listed; ~2 ms at "
-          "256K/8 ranks at ~900 GB/s).\n")
+          "replicated. `zigzag`: rank r owns contiguous chunks r and 2G-1-r of 2G chunks "
+          "(`fpb_*_zigzag`), K/V replicated. The O+LSE all-gather after the kernels is not timed "
+          "(bytes listed; ~2 ms at 256K/8 ranks at ~900 GB/s).\n")
     print("| L | G | partition | step ms (max over ranks) | per-rank step ms | job eff. TFLOP/s | "
           "all-gather bytes per rank |")
     print("|" + "---|" * 7)
@@ -156,7 +157,7 @@ def main():
             out.write(line + "\n")
             out.flush()
         for G in (2, 4, 8):
-            for part in ("kv_group", "rows"):
+            for part in ("kv_group", "rows", "zigzag"):
                 per_rank = []
                 for rank in range(G):
                     if part == "kv_group":
@@ -164,8 +165,9 @@ def main():
                         ql, kl, vl = (x.contiguous() for x in shard.local_slices(q, k, v, s))
                         td, ta, _, vis = stage(ql, kl, vl, cfg, grid, tau, reps)
                     else:
-                        td, ta, _, vis = stage(q, k, v, cfg, grid, tau, reps,
-                                               rows=shard.row_shard(G, rank))
+                        rows = (shard.row_shard(G, rank) if part == "rows"
+                                else shard.zigzag_shard(G, rank))
+                        td, ta, _, vis = stage(q, k, v, cfg, grid, tau, reps, rows=rows)
                     per_rank.append((td + ta, td, ta, vis))
                 worst = max(per_rank)
                 gather = (G - 1) / G * HQ * L * (D * 2 + 4)  # bf16 O + fp32 LSE received per rank

@@ -11,7 +11,8 @@
 //   TMEM (512 cols): S0 | S1 | O0 | O1; P (bf16) is written back over S and read by the PV MMA
 //   straight from TMEM (ts form).  Issue order per slot unit: PV(j-1) then QK(j) — in-order
 //   tcgen05 execution makes the S/P aliasing safe.
-//   SMEM: Q0, Q1 (32 KiB each) + a 5-tile K/V ring shared by both slots, filled by TMA in exactly
+//   SMEM: Q0, Q1 (32 KiB each) + a 5-tile K/V ring shared by both slots, filled by TMA (one 4-D
+//   box per 128 x 128 tile: both 64-column SW128 halves in one instruction) in exactly
 //   the MMA consumption order (both warps run the same deterministic unit schedule).  At the end
 //   of an item the slot's Q tile is the staging buffer of the O tile, written by one TMA store.
 //   Compacted plan rows live in a global scratch (L2-resident), not in SMEM.
@@ -265,9 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) {
         const uint32_t fb = smem_u32(&s.kv_full[r]);
         mbar_arrive_expect_tx(fb, kTile);
-        for (int a = 0; a < 2; ++a)
-          tma_load_3d_hint(smem_u32(s.ring[r]) + a * (kTile / 2), map, fb, a * 64, row, plane,
-                           pol_kv);
+        tma_load_4d_hint(smem_u32(s.ring[r]), map, fb, 0, row, 0, plane, pol_kv);  // whole tile
       }
       __syncwarp();
       ++kvc;
@@ -304,9 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) {
             const uint32_t qb = smem_u32(&s.q_full[sl]);
             mbar_arrive_expect_tx(qb, kTile);
-            for (int a = 0; a < 2; ++a)
-              tma_load_3d_hint(smem_u32(s.q[sl]) + a * (kTile / 2), &tm_q, qb, a * 64,
-                               qi * kBlock, z * D.Hq + h, pol_q);
+            tma_load_4d_hint(smem_u32(s.q[sl]), &tm_q, qb, 0, qi * kBlock, 0, z * D.Hq + h, pol_q);
           }
           __syncwarp();
           ++S.qc;
@@ -630,9 +627,9 @@ cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __n
                                 bool out_bf16, void* out, float* lse, unsigned long long* visits,
                                 int32_t* plan_error, int* sched, uint16_t* lists, cudaStream_t s) {
   CUtensorMap tm_q, tm_k, tm_v, tm_o;
-  if (!make_tmap_rows128(&tm_q, Q, D.L, (uint64_t)D.Z * D.Hq) ||
-      !make_tmap_rows128(&tm_k, K, D.L, (uint64_t)D.Z * D.Hkv) ||
-      !make_tmap_rows128(&tm_v, V, D.L, (uint64_t)D.Z * D.Hkv) ||
+  if (!make_tmap_tiles128(&tm_q, Q, D.L, (uint64_t)D.Z * D.Hq) ||
+      !make_tmap_tiles128(&tm_k, K, D.L, (uint64_t)D.Z * D.Hkv) ||
+      !make_tmap_tiles128(&tm_v, V, D.L, (uint64_t)D.Z * D.Hkv) ||
       !make_tmap_rows128(&tm_o, out_bf16 ? out : Q, D.L, (uint64_t)D.Z * D.Hq))
     return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(sched, 0, sizeof(int), s);

@@ -94,5 +94,6 @@ cudaError_t launch_exact(const Dims& D, bool bf16_in, const void* Q, const void*
 
 // tensor maps (abi.cu)
 bool make_tmap_rows128(CUtensorMap* map, const void* base, uint64_t rows, uint64_t planes);
+bool make_tmap_tiles128(CUtensorMap* map, const void* base, uint64_t rows, uint64_t planes);
 
 }  // namespace fpb

@@ -82,6 +82,11 @@ class Oracle:
         gp("pipeline_threads").argtypes = [_p, _p, _p, _u64, _u64, _u64, _u64, _u64, _u32, _f32,
                                            _u32, _u32, _f32, _f32, _p, _i32, _i32, _p, _p, _p]
         gp("pipeline_threads").restype = C.c_double
+        if pre == "ref_":
+            gp("pipeline_detail").argtypes = [_p, _p, _p, _u64, _u64, _u64, _u64, _u64, _u32,
+                                              _f32, _u32, _u32, _f32, _f32, _p, _i32, _i32, _p,
+                                              _p, _p, _p, _p, _p, _p, _p]
+            gp("pipeline_detail").restype = C.c_double
         gp("topk_select").argtypes = [_p, _u64, _u64, _u32, _u32, _u32, _u32, _u32, _p]
         gp("topp_select").argtypes = [_p, _u64, _u64, _u32, _f32, _u32, _u32, _u32, _p]
         if pre == "or_":
@@ -307,6 +312,40 @@ class Oracle:
         if secs < 0:
             raise ValueError("pipeline failed")
         return secs, out, lse, vis.value
+
+    def pipeline_detail(self, q, k, v, B, alpha, sink_tokens, window_tokens, tau, eps, heads,
+                        threads, row_keep=None, attend=True):
+        """Reference pipeline per (z*Hq + h) slice in `heads`, returning everything the full-size
+        parity tests compare (reference shim only).
+
+        row_keep: optional bool[M]; attention runs only on those query-block rows (the other
+        rows' counts are zeroed before block_sparse_attention, so their out / lse are NaN / -inf).
+        Returns dict(secs, score[n,M,M], idx[n,M,M], counts[n,M], comparisons, out[n,L,d],
+        lse[n,L], visits)."""
+        f = self._ref_only("pipeline_detail")
+        q, k, v = _f(q), _f(k), _f(v)
+        Z, Hq, L, d = q.shape
+        Hkv = k.shape[1]
+        M, _ = self.grid(L, B)
+        heads = np.ascontiguousarray(heads, dtype=np.int32)
+        n = len(heads)
+        keep = None
+        if row_keep is not None or not attend:
+            keep = np.zeros(M, np.uint8) if not attend else \
+                np.ascontiguousarray(row_keep, dtype=np.uint8)
+        score = np.empty((n, M, M), np.float32)
+        idx = np.empty((n, M, M), np.int32)
+        counts = np.empty((n, M), np.int32)
+        out = np.empty((n, L, d), np.float32) if attend else None
+        lse = np.empty((n, L), np.float32) if attend else None
+        cmp, vis = C.c_uint64(0), C.c_uint64(0)
+        secs = f(_ptr(q), _ptr(k), _ptr(v), Z, Hq, Hkv, L, d, B, alpha, sink_tokens,
+                 window_tokens, tau, eps, _ptr(heads), n, threads, _ptr(keep), _ptr(score),
+                 _ptr(idx), _ptr(counts), C.byref(cmp), _ptr(out), _ptr(lse), C.byref(vis))
+        if secs < 0:
+            raise ValueError("reference pipeline failed")
+        return dict(secs=secs, score=score, idx=idx, counts=counts, comparisons=cmp.value,
+                    out=out, lse=lse, visits=vis.value)
 
     # ------------------------------------------------------------------ reference-only (CLI pins)
     def _ref_only(self, name):

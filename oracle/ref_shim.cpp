@@ -311,4 +311,67 @@ double ref_pipeline_threads(const float* q, const float* k, const float* v, uint
   return err ? -1.0 : secs;
 }
 
+// The same reference pipeline, also returning what the full-size parity tests compare: per sampled
+// slice s the score map (M x N), the plan (idx M x N, counts M) exactly as compress_indices wrote
+// them, and out / lse.  `row_keep` (M bytes, nullable) bounds the CPU cost at long L: before
+// block_sparse_attention the counts of rows with row_keep[i] == 0 are set to 0 (the reference
+// then writes NaN / -inf there, attention.hpp:119-126); the returned counts are the original ones.
+double ref_pipeline_detail(const float* q, const float* k, const float* v, uint64_t Z,
+                           uint64_t Hq, uint64_t Hkv, uint64_t L, uint64_t d, uint32_t B,
+                           float alpha, uint32_t sink_tokens, uint32_t window_tokens, float tau,
+                           float eps, const int32_t* head_list, int n_heads, int threads,
+                           const uint8_t* row_keep, float* score, int32_t* idx, int32_t* counts,
+                           uint64_t* comparisons, float* out, float* lse, uint64_t* visits) {
+  PipelineConfig cfg;
+  cfg.block_size = B;
+  cfg.alpha = alpha;
+  cfg.sink_tokens = sink_tokens;
+  cfg.window_tokens = window_tokens;
+  cfg.epsilon = eps;
+  const BlockGrid grid = make_block_grid(L, B);
+  const uint64_t Ld = L * d, MN = (uint64_t)grid.num_query_blocks * grid.num_key_blocks;
+  const uint32_t M = grid.num_query_blocks;
+  std::atomic<int> next{0}, err{0};
+  std::atomic<uint64_t> vis_total{0}, cmp_total{0};
+  auto worker = [&] {
+    for (;;) {
+      const int s = next.fetch_add(1);
+      if (s >= n_heads) break;
+      const int rc = guarded([&] {
+        const uint64_t zh = static_cast<uint64_t>(head_list[s]);
+        const uint64_t z = zh / Hq, h = zh % Hq, kvh = z * Hkv + h / (Hq / Hkv);
+        const auto qs = batch(q + zh * Ld, 1, 1, L, d, Role::kQuery);
+        const auto ks = batch(k + kvh * Ld, 1, 1, L, d, Role::kKey);
+        const auto vs = batch(v + kvh * Ld, 1, 1, L, d, Role::kValue);
+        const auto map = discover(qs, ks, grid, tau, eps);
+        SelectionStats sst;
+        const auto mask = max_threshold_mask(map, cfg, &sst);
+        auto plan = compress_indices(mask);
+        cmp_total += sst.score_comparisons;
+        if (score) std::memcpy(score + s * MN, map.score.data(), sizeof(float) * MN);
+        if (idx) std::memcpy(idx + s * MN, plan.indices.data(), sizeof(int32_t) * MN);
+        if (counts) std::memcpy(counts + s * (uint64_t)M, plan.counts.data(), sizeof(int32_t) * M);
+        if (row_keep)
+          for (uint32_t i = 0; i < M; ++i)
+            if (!row_keep[i]) plan.counts.data()[i] = 0;
+        AttentionStats stats;
+        const auto res = block_sparse_attention(qs, ks, vs, plan, grid, tau, &stats);
+        if (out) std::memcpy(out + static_cast<uint64_t>(s) * Ld, res.out.data(), sizeof(float) * Ld);
+        if (lse) std::memcpy(lse + static_cast<uint64_t>(s) * L, res.lse.data(), sizeof(float) * L);
+        vis_total += stats.block_visits;
+      });
+      if (rc) err = rc;
+    }
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int i = 0; i < (threads < 1 ? 1 : threads); ++i) pool.emplace_back(worker);
+  for (auto& t : pool) t.join();
+  const double secs =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (visits) *visits = vis_total.load();
+  if (comparisons) *comparisons = cmp_total.load();
+  return err ? -1.0 : secs;
+}
+
 }  // extern "C"

@@ -696,12 +696,15 @@ class PrefillRunner:
             self.attend()
         torch.cuda.current_stream(self.q.device).wait_stream(side)
         torch.cuda.synchronize(self.q.device)
-        g_disc, g_attn = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        # keep_graph: the cudaGraph_t stays queryable (kernel_nodes) after instantiation
+        g_disc, g_attn = torch.cuda.CUDAGraph(keep_graph=True), torch.cuda.CUDAGraph(keep_graph=True)
         # relaxed: the launch helpers query device attributes while the stream is capturing
         with torch.cuda.graph(g_disc, capture_error_mode="relaxed"):
             self.discover()
         with torch.cuda.graph(g_attn, capture_error_mode="relaxed"):
             self.attend()
+        g_disc.instantiate()
+        g_attn.instantiate()
         self.graphs = (g_disc, g_attn)
         return self
 

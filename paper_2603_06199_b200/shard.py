@@ -64,21 +64,44 @@ def local_slices(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, s: HeadShard
             v[:, s.kv_lo:s.kv_hi].contiguous())
 
 
+def _all_gather(dst: torch.Tensor, src: torch.Tensor, group=None) -> None:
+    """all_gather_into_tensor; over gloo (CPU tests, the shared-GPU test mode) device tensors
+    are staged through host memory."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    src = src.reshape(1, -1)  # rank-major chunks along dim 0 (gloo requires it)
+    if dist.get_backend(group) == "gloo" and src.is_cuda:
+        tmp = torch.empty((world, src.shape[1]), dtype=dst.dtype)
+        dist.all_gather_into_tensor(tmp, src.cpu(), group=group)
+        dst.copy_(tmp.view(dst.shape))
+    else:
+        dist.all_gather_into_tensor(dst.view(world, -1), src, group=group)
+
+
 def gather_heads(out_local: torch.Tensor, lse_local: torch.Tensor, Hq: int, Hkv: int,
-                 group=None):
-    """All-gather per-rank (Z x hq_local x L x d, Z x hq_local x L) along the head axis."""
+                 group=None, out: torch.Tensor | None = None, lse: torch.Tensor | None = None):
+    """All-gather per-rank (Z x hq_local x L x d, Z x hq_local x L) along the head axis.
+
+    For Z = 1 the ranks' head ranges are contiguous and ascending, so the collective writes the
+    final Z x Hq x L x d layout directly (no staging copy); `out` / `lse` may be preallocated."""
     import torch.distributed as dist
     world = dist.get_world_size(group)
     Z, hl, L, d = out_local.shape
+    if out is None:
+        out = torch.empty((Z, Hq, L, d), dtype=out_local.dtype, device=out_local.device)
+    if lse is None:
+        lse = torch.empty((Z, Hq, L), dtype=lse_local.dtype, device=lse_local.device)
+    order = [kv_group_shard(Hq, Hkv, world, r).q_lo for r in range(world)]
+    if Z == 1 and order == [r * hl for r in range(world)] and world * hl == Hq:
+        _all_gather(out, out_local.contiguous(), group)
+        _all_gather(lse, lse_local.contiguous(), group)
+        return out, lse
     # head-major staging so one all_gather_into_tensor moves every rank's block contiguously
     ob = torch.empty((world * Z, hl, L, d), dtype=out_local.dtype, device=out_local.device)
     lb = torch.empty((world * Z, hl, L), dtype=lse_local.dtype, device=lse_local.device)
-    dist.all_gather_into_tensor(ob, out_local.contiguous(), group=group)
-    dist.all_gather_into_tensor(lb, lse_local.contiguous(), group=group)
+    _all_gather(ob, out_local.contiguous(), group)
+    _all_gather(lb, lse_local.contiguous(), group)
     ob, lb = ob.view(world, Z, hl, L, d), lb.view(world, Z, hl, L)
-    order = [kv_group_shard(Hq, Hkv, world, r).q_lo for r in range(world)]
-    out = torch.empty((Z, Hq, L, d), dtype=out_local.dtype, device=out_local.device)
-    lse = torch.empty((Z, Hq, L), dtype=lse_local.dtype, device=lse_local.device)
     for r, q0 in enumerate(order):
         out[:, q0:q0 + hl] = ob[r]
         lse[:, q0:q0 + hl] = lb[r]
@@ -137,7 +160,7 @@ def gather_zigzag(out: torch.Tensor, lse: torch.Tensor, block: int, group=None):
         xc = x.view((Z, H, 2 * world, c * block) + tuple(x.shape[3:]))
         mine = torch.stack((xc[:, :, rank], xc[:, :, 2 * world - 1 - rank]), dim=2).contiguous()
         allr = torch.empty((world * Z,) + tuple(mine.shape[1:]), dtype=x.dtype, device=x.device)
-        dist.all_gather_into_tensor(allr, mine, group=group)
+        _all_gather(allr, mine, group)
         allr = allr.view((world,) + tuple(mine.shape))  # rank, Z, H, 2, cB, ...
         chunks = [allr[r, :, :, 0] for r in range(world)] + \
                  [allr[r, :, :, 1] for r in reversed(range(world))]
@@ -170,7 +193,7 @@ def gather_rows(out: torch.Tensor, lse: torch.Tensor, block: int, group=None):
         mine = xb[:, :, :, rank].contiguous()
         allr = torch.empty((world * mine.shape[0],) + tuple(mine.shape[1:]), dtype=x.dtype,
                            device=x.device)
-        dist.all_gather_into_tensor(allr, mine, group=group)
+        _all_gather(allr, mine, group)
         full = allr.view((world,) + tuple(mine.shape)).movedim(0, 3).contiguous()
         full = full.view((x.shape[0], x.shape[1], -1) + tuple(x.shape[3:]))[:, :, :L]
         res.append(full.contiguous())

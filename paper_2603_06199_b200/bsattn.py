@@ -12,6 +12,7 @@ per Q head and Q head h reads KV head h // (Hq // Hkv).
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass
 
 import torch
@@ -220,19 +221,26 @@ def problem(q_shape, hkv: int, config: PipelineConfig | None = None, tau: float 
 
 
 _ws_cache: dict = {}
+_ws_lock = threading.Lock()
 
 
 def workspace(p: _abi.Problem, dtype_code: int, device) -> tuple[torch.Tensor | None, int]:
-    """Grow-only per-device scratch (fpb_workspace_bytes); no allocation on repeat calls."""
+    """Grow-only scratch (fpb_workspace_bytes) per (device, current stream); no allocation on
+    repeat calls.  The kernels keep their work-queue counters and list scratch in it, so calls on
+    different streams must not share one buffer (reentrancy across streams); calls on
+    one stream are ordered by the stream.  The buffer is allocated while its stream is current,
+    so the caching allocator's reuse after a grow is ordered on that same stream."""
     n = C.c_size_t(0)
     _raise(_abi.lib().fpb_workspace_bytes(C.byref(p), dtype_code, C.byref(n)), "workspace")
     if n.value == 0:
         return None, 0
-    key = torch.device(device)
-    buf = _ws_cache.get(key)
-    if buf is None or buf.numel() < n.value:
-        buf = torch.empty(n.value, dtype=torch.uint8, device=device)
-        _ws_cache[key] = buf
+    dev = torch.device(device)
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    with _ws_lock:
+        buf = _ws_cache.get(key)
+        if buf is None or buf.numel() < n.value:
+            buf = torch.empty(n.value, dtype=torch.uint8, device=dev)
+            _ws_cache[key] = buf
     return buf, n.value
 
 

@@ -155,6 +155,7 @@ size_t kbar_split_bytes(const Dims& D) { return 2ull * D.Z * D.Hkv * D.M * kHead
 //                     attention: [Q hi/lo][K hi/lo][V bf16] if fp32
 //   generic discover: [pooled][energy][local_max][score][mask]
 constexpr size_t kSchedBytes = 1024;
+constexpr size_t kMaxSmemPerCta = 227 * 1024;  // sm_100 opt-in dynamic shared memory per CTA
 size_t ws_discover(const Dims& D, fpb_dtype t) {
   if (!tc_path(D))
     return align_up(pooled_bytes(D)) + 3 * align_up(map_elems(D) * 4) + align_up(map_elems(D));
@@ -556,6 +557,12 @@ static int attention_common(const fpb_problem* p, fpb_dtype dtype, const void* Q
                       *k = static_cast<const __nv_bfloat16*>(K),
                       *v = static_cast<const __nv_bfloat16*>(V);
   if (dtype == FPB_F32) {
+    // the split-precision one-tile kernel keeps its block list in shared memory
+    if (attention_f32_smem_bytes(D) > kMaxSmemPerCta)
+      return fail(FPB_EVALIDATION,
+                  "fp32 inputs support at most %d key blocks (got %d); pass bf16 for longer "
+                  "sequences",
+                  (int)((kMaxSmemPerCta - attention_f32_smem_bytes(Dims{})) / sizeof(int)), D.M);
     uint8_t* w = static_cast<uint8_t*>(workspace) + kSchedBytes + align_up(attention_list_bytes(D));
     __nv_bfloat16* q2 = reinterpret_cast<__nv_bfloat16*>(w);
     __nv_bfloat16* k2 = reinterpret_cast<__nv_bfloat16*>(w + align_up(2 * q_elems(D) * 2));
@@ -632,7 +639,9 @@ struct Arena {
   cudaStream_t stream = nullptr;
   cudaStream_t s_in = nullptr, s_out = nullptr;  // copy streams of the pipelined prefill
   cudaStream_t s_c2 = nullptr;                     // second compute stream of the prefill
+  std::vector<cudaEvent_t> events;                 // grow-only pool of the prefill's chunk events
   ~Arena() {
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
     if (ptr) cudaFree(ptr);
     if (stream) cudaStreamDestroy(stream);
     if (s_in) cudaStreamDestroy(s_in);
@@ -641,6 +650,27 @@ struct Arena {
   }
 };
 thread_local Arena g_arena;
+
+// Drains every arena stream when a host entry point returns, so no async copy of the caller's
+// host buffers (or kernel on the arena) is still in flight after an error return; on the success
+// path the streams are already idle and this is a no-op.
+struct ArenaDrain {
+  ~ArenaDrain() {
+    for (cudaStream_t s : {g_arena.stream, g_arena.s_in, g_arena.s_out, g_arena.s_c2})
+      if (s) cudaStreamSynchronize(s);
+  }
+};
+
+// n timing-disabled events from the arena's pool (created once, reused by every call)
+int arena_events(size_t n, cudaEvent_t** out) {
+  while (g_arena.events.size() < n) {
+    cudaEvent_t e;
+    FPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    g_arena.events.push_back(e);
+  }
+  *out = g_arena.events.data();
+  return FPB_OK;
+}
 
 int arena_get(size_t bytes, uint8_t** out, cudaStream_t* st) {
   if (!g_arena.stream) FPB_CUDA(cudaStreamCreateWithFlags(&g_arena.stream, cudaStreamNonBlocking));
@@ -675,6 +705,7 @@ extern "C" {
 
 int fpb_host_pool_keys(const fpb_problem* p, fpb_dtype dtype, const void* K, float* pooled) {
   Dims D;
+  ArenaDrain drain;  // error returns leave nothing in flight
   int rc = resolve(p, &D);
   if (rc || (rc = check_dtype(dtype))) return rc;
   if (!K || !pooled) return fail(FPB_EUSAGE, "null pointer");
@@ -695,6 +726,7 @@ int fpb_host_pool_keys(const fpb_problem* p, fpb_dtype dtype, const void* K, flo
 int fpb_host_approx_block_scores(const fpb_problem* p, fpb_dtype dtype, const void* Q,
                                  const float* pooled, float* energy, float* local_max) {
   Dims D;
+  ArenaDrain drain;  // error returns leave nothing in flight
   int rc = resolve(p, &D);
   if (rc || (rc = check_dtype(dtype))) return rc;
   if (!Q || !pooled || !energy || !local_max) return fail(FPB_EUSAGE, "null pointer");
@@ -722,6 +754,7 @@ int fpb_host_approx_block_scores(const fpb_problem* p, fpb_dtype dtype, const vo
 int fpb_host_normalize_block_scores(const fpb_problem* p, const float* energy,
                                     const float* local_max, float* score) {
   Dims D;
+  ArenaDrain drain;  // error returns leave nothing in flight
   int rc = resolve(p, &D);
   if (rc) return rc;
   if (!energy || !local_max || !score) return fail(FPB_EUSAGE, "null pointer");
@@ -744,6 +777,7 @@ int fpb_host_normalize_block_scores(const fpb_problem* p, const float* energy,
 int fpb_host_discover(const fpb_problem* p, fpb_dtype dtype, const void* Q, const void* K,
                       float* energy, float* local_max, float* score) {
   Dims D;
+  ArenaDrain drain;  // error returns leave nothing in flight
   int rc = resolve(p, &D);
   if (rc || (rc = check_dtype(dtype))) return rc;
   if (!Q || !K || !score) return fail(FPB_EUSAGE, "null pointer");
@@ -775,6 +809,7 @@ int fpb_host_discover(const fpb_problem* p, fpb_dtype dtype, const void* Q, cons
 int fpb_host_max_threshold_mask(const fpb_problem* p, const float* score, uint8_t* mask,
                                 unsigned long long* comparisons) {
   Dims D;
+  ArenaDrain drain;  // error returns leave nothing in flight
   int rc = resolve(p, &D);
   if (rc) return rc;
   if (!score || !mask) return fail(FPB_EUSAGE, "null pointer");
@@ -800,6 +835,7 @@ int fpb_host_max_threshold_mask(const fpb_problem* p, const float* score, uint8_
 static int host_sort_select(const fpb_problem* p, const float* score, int mode, int32_t k,
                             float top_p, uint8_t* mask) {
   Dims D;
+  ArenaDrain drain;  // error returns leave nothing in flight
   int rc = resolve(p, &D);
   if (rc) return rc;
   if (!score || !mask) return fail(FPB_EUSAGE, "null pointer");
@@ -830,6 +866,7 @@ int fpb_host_discover_method(const fpb_problem* p, fpb_dtype dtype, int method, 
   if (method == 0) return fpb_host_discover(p, dtype, Q, K, energy, local_max, score);
   if (method != 1 && method != 2) return fail(FPB_EUSAGE, "unknown discovery method %d", method);
   Dims D;
+  ArenaDrain drain;  // error returns leave nothing in flight
   int rc = resolve(p, &D);
   if (rc || (rc = check_dtype(dtype))) return rc;
   if (!Q || !K || !energy || !local_max || !score) return fail(FPB_EUSAGE, "null pointer");
@@ -862,6 +899,7 @@ int fpb_host_discover_method(const fpb_problem* p, fpb_dtype dtype, int method, 
 int fpb_host_compress_indices(const fpb_problem* p, const uint8_t* mask, int32_t* idx,
                               int32_t* counts) {
   Dims D;
+  ArenaDrain drain;  // error returns leave nothing in flight
   int rc = resolve(p, &D);
   if (rc) return rc;
   if (!mask || !idx || !counts) return fail(FPB_EUSAGE, "null pointer");
@@ -888,6 +926,7 @@ static int host_attention(const fpb_problem* p, fpb_dtype dtype, const void* Q, 
                           fpb_dtype out_dtype, void* out, float* lse,
                           unsigned long long* visits) {
   Dims D;
+  ArenaDrain drain;  // error returns leave nothing in flight
   int rc = resolve(p, &D);
   if (rc || (rc = check_dtype(dtype)) || (rc = check_dtype(out_dtype))) return rc;
   if (!Q || !K || !V || !out || !lse) return fail(FPB_EUSAGE, "null pointer");
@@ -958,6 +997,7 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
   // Pipelined over chunks of Q heads (each inside one KV group): H2D of chunk c+1, the kernels of
   // chunk c and the D2H of chunk c-1 run concurrently on three streams (PCIe is full duplex).
   Dims D;
+  ArenaDrain drain;  // error returns leave nothing in flight
   int rc = resolve(p, &D);
   if (rc || (rc = check_dtype(dtype)) || (rc = check_dtype(out_dtype))) return rc;
   if (!Q || !K || !V || !out || !lse) return fail(FPB_EUSAGE, "null pointer");
@@ -1021,19 +1061,13 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
     di[i] = c.take<int32_t>(sib);
     dc[i] = c.take<int32_t>(scb);
   }
-  std::vector<cudaEvent_t> ev_in(nch), ev_done(nch);
-  for (int i = 0; i < nch; ++i) {
-    FPB_CUDA(cudaEventCreateWithFlags(&ev_in[i], cudaEventDisableTiming));
-    FPB_CUDA(cudaEventCreateWithFlags(&ev_done[i], cudaEventDisableTiming));
-  }
+  cudaEvent_t* evp;
+  if ((rc = arena_events(2 * (size_t)nch + 1, &evp))) return rc;
+  cudaEvent_t *ev_in = evp, *ev_done = evp + nch, e0 = evp[2 * nch];
   FPB_CUDA(cudaMemsetAsync(dvis, 0, 8 * nch, st));
-  {  // the second compute stream starts after the memset (and any earlier use of the arena)
-    cudaEvent_t e0;
-    FPB_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
-    FPB_CUDA(cudaEventRecord(e0, st));
-    FPB_CUDA(cudaStreamWaitEvent(sc[1], e0, 0));
-    cudaEventDestroy(e0);
-  }
+  // the second compute stream starts after the memset (and any earlier use of the arena)
+  FPB_CUDA(cudaEventRecord(e0, st));
+  FPB_CUDA(cudaStreamWaitEvent(sc[1], e0, 0));
   // FPB_E2E_TRACE=1: per-chunk timeline (H2D done / kernels done / D2H done) on stderr
   static const bool trace = getenv("FPB_E2E_TRACE") != nullptr;
   std::vector<cudaEvent_t> tr_in, tr_k, tr_out;
@@ -1122,10 +1156,6 @@ int fpb_host_prefill(const fpb_problem* p, fpb_dtype dtype, const void* Q, const
       cudaEventDestroy(tr_out[i]);
     }
     cudaEventDestroy(tr0);
-  }
-  for (int i = 0; i < nch; ++i) {
-    cudaEventDestroy(ev_in[i]);
-    cudaEventDestroy(ev_done[i]);
   }
   if (visits)
     for (auto x : vis) *visits += x;

@@ -110,7 +110,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (dense) {
     if (threadIdx.x == 0) s.nblk = qi + 1;
   } else {
-    const int C = prm.counts[((size_t)z * D.M + qi) * D.Hq + h];
+    int C = prm.counts[((size_t)z * D.M + qi) * D.Hq + h];
+    if (C > N) {  // malformed plan: a row has N slots, never read past it
+      if (threadIdx.x == 0 && prm.plan_error) atomicExch(prm.plan_error, 1);
+      C = N;
+    }
     const size_t prow = ((size_t)z * D.M + qi) * (size_t)N;
     int base = 0;
     for (int s0 = 0; s0 < C; s0 += kThreads) {
@@ -373,6 +377,10 @@ cudaError_t launch_attention(const Dims& D, int splits, const __nv_bfloat16* Q,
     return cudaErrorInvalidValue;
   AttnParams prm{D, idx, counts, out, lse, visits, plan_error, out_bf16 ? 1 : 0};
   return launch_ns<2>(D, tm_q, tm_k, tm_v, prm, s);
+}
+
+size_t attention_f32_smem_bytes(const Dims& D) {
+  return sizeof(AttnSmem<2>) + 1024 + sizeof(int) * (size_t)D.M;
 }
 
 size_t attention_list_bytes(const Dims& D) { return (size_t)256 * 4 * D.M * sizeof(uint16_t); }

@@ -200,7 +200,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (dense) {
             nblk = qi + 1;
           } else {
-            const int C = prm.counts[((size_t)z * D.M + qi) * D.Hq + h];
+            int C = prm.counts[((size_t)z * D.M + qi) * D.Hq + h];
+            if (C > N) {  // a row has N slots: more is a malformed plan, never read past it
+              if (lane == 0 && prm.plan_error) atomicExch(prm.plan_error, 1);
+              C = N;
+            }
             const size_t prow = ((size_t)z * D.M + qi) * (size_t)N;
             uint16_t* lst = list_of(sl, p);
             for (int s0 = 0; s0 < C; s0 += 32) {  // attention.hpp:76-81: range-check each slot

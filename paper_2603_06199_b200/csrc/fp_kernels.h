@@ -69,6 +69,7 @@ cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __n
                                 int32_t* plan_error, int* sched, uint16_t* lists, cudaStream_t s);
 // bytes of the compacted-plan scratch launch_attention needs (grid x 2 slots x 2 bufs x M x u16)
 size_t attention_list_bytes(const Dims& D);
+size_t attention_f32_smem_bytes(const Dims& D);  // fp32-input kernel (attention.cu)
 
 // generic.cu — SIMT kernels for shapes outside the tensor-core tile (d != 128 or B != 128)
 cudaError_t g_launch_pool(const GenDims& G, bool bf16_in, const void* K, float* pooled,

@@ -112,7 +112,11 @@ __global__ void g_attention_kernel(GenDims G, const T* __restrict__ Q, const T* 
   const int rows = (qi + 1 == G.M) ? G.last_len : G.B;
   const int N = G.M;
   const bool dense = idx == nullptr;
-  const int C = dense ? qi + 1 : counts[((size_t)z * G.M + qi) * G.Hq + h];
+  int C = dense ? qi + 1 : counts[((size_t)z * G.M + qi) * G.Hq + h];
+  if (C > N) {  // malformed plan: a row has N slots, never read past it
+    if (threadIdx.x == 0 && plan_error) atomicExch(plan_error, 1);
+    C = N;
+  }
   const size_t kvh = (size_t)z * G.Hkv + h / G.group;
   // per-thread scratch: acc[d] + logits[B]
   for (int r = threadIdx.x; r < rows; r += blockDim.x) {

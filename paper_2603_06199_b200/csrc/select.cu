@@ -117,7 +117,7 @@ __global__ void fill_plan_kernel(Dims D, int32_t* __restrict__ idx) {
   const int rows = D.Z * D.Mr;
   const int4 f = make_int4(D.M, D.M, D.M, D.M);
   for (int r = blockIdx.y; r < rows; r += gridDim.y) {
-    const int z = r / D.Mr, I = D.rb + D.rs * (r % D.Mr);
+    const int z = r / D.Mr, I = owned_row(D, r % D.Mr);  // interleaved, zigzag or all rows
     int32_t* row = idx + ((size_t)z * D.M + I) * row_ints;
     int4* row4 = reinterpret_cast<int4*>(row);
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < row_vec;

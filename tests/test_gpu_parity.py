@@ -62,9 +62,13 @@ def test_discover_maps(fp, port, case):
     # causal entries: local max (base-2 logit units) and scores close to the fp32 reference
     dl = np.abs(glm - lm)[np.broadcast_to(tri, lm.shape)]
     assert dl.max() <= 2e-4 * max(1.0, np.abs(lm[np.broadcast_to(tri, lm.shape)]).max())
+    # scores: relative 5e-5 (SURVEY §7 targets the reference's own 1e-5 energy bar,
+    # test_discovery.cpp:114-116; k̄ enters as a 16-significant-bit hi+lo split and exp2 is
+    # ex2.approx, so a few ulps more are allowed, far inside the 1e-4 mask band)
     rs = np.abs(gsc - sc) / np.maximum(sc, 1e-30)
     big = np.broadcast_to(tri, sc.shape) & (sc > 1e-6)
-    assert rs[big].max() <= 1e-3, rs[big].max()
+    print(f"score rel err max {rs[big].max():.2e} mean {rs[big].mean():.2e}")
+    assert rs[big].max() <= 5e-5, rs[big].max()
 
 
 @pytest.mark.parametrize("alpha", [0.0, 0.05, 0.12, 0.5, 1.0])

@@ -73,6 +73,29 @@ def test_zigzag_shards_equal_whole(fp, world):
     assert bool((seen == 1).all())
 
 
+@pytest.mark.parametrize("part", ["rows", "zigzag"])
+def test_long_row_shards_fill_owned_rows(fp, part):
+    """M >= 1024 key blocks: the plan rows are prefilled with N by fill_plan_kernel and the fused
+    epilogue then writes only the active slots.  The prefill must hit exactly the rank's owned rows
+    (interleaved or zigzag), so every owned row -- fill slots included -- equals the unsharded
+    plan row (selection.hpp:176-192: slots >= C hold N)."""
+    Z, Hq, Hkv, L = 1, 2, 1, 1030 * 128 - 5  # M = 1030, ragged last block
+    q, k, _ = fp.workload.composite(21, Z, Hq, Hkv, L, device="cuda")
+    cfg = fp.PipelineConfig(alpha=0.12)
+    M = fp.make_block_grid(L, 128).num_query_blocks
+    plan = fp.discover_select(q, k, cfg)[0]
+    world = 3
+    for rank in range(world):
+        if part == "rows":
+            rows, own = (rank, world), list(range(rank, M, world))
+        else:
+            rows, own = fp.shard.zigzag_shard(world, rank), fp.shard.zigzag_blocks(M, world, rank)
+        pr = fp.discover_select(q, k, cfg, rows=rows)[0]
+        own_t = torch.as_tensor(own, device="cuda")
+        assert torch.equal(pr.counts[:, own_t], plan.counts[:, own_t]), (part, rank)
+        assert torch.equal(pr.indices[:, own_t], plan.indices[:, own_t]), (part, rank)
+
+
 def test_zigzag_runner_and_validation(fp):
     """PrefillRunner graphs on a zigzag shard reproduce the direct calls; rank outside
     [0, world) is a ValidationError."""

@@ -3,8 +3,9 @@
 
 usage: python tools/ncu_summary.py gpurun_out/r1_attn.ncu-rep [more.ncu-rep ...]
        python tools/ncu_summary.py --traffic KERNEL 'CONFIG_JSON' rep.ncu-rep
-           records that kernel's per-launch DRAM bytes (read + write) in profiles/ncu_traffic.json,
-           which bench.py reports as roofline.traffic when its config matches CONFIG_JSON.
+           records that kernel's per-launch DRAM bytes (read + write) in profiles/ncu_traffic.json
+           (one record per config), which bench.py reports as roofline.traffic / the sweep's
+           attn_traffic / disc_traffic when its config matches CONFIG_JSON.
 """
 import json
 import os
@@ -86,7 +87,11 @@ def traffic(path, kernel, cfg):
         dest = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                             "profiles", "ncu_traffic.json")
         data = json.load(open(dest)) if os.path.exists(dest) else {}
-        data[kernel] = {"dram_bytes": tot, "config": cfg, "capture": os.path.basename(path)}
+        recs = data.get(kernel, [])
+        recs = recs if isinstance(recs, list) else [recs]
+        recs = [x for x in recs if x.get("config") != cfg]  # one record per config
+        recs.append({"dram_bytes": tot, "config": cfg, "capture": os.path.basename(path)})
+        data[kernel] = recs
         with open(dest, "w") as f:
             json.dump(data, f, indent=1)
         return tot

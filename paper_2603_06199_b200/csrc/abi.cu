@@ -232,12 +232,13 @@ bool make_tmap_rows128(CUtensorMap* map, const void* base, uint64_t rows, uint64
 // Whole 128 x 128 bf16 tile in ONE TMA: the two 64-column SW128 halves become a third box
 // dimension (dims: 64 columns, rows, 2 halves, planes; the half stride, 128 B, is below the row
 // stride), so shared memory receives [half][row][64] exactly as two 3-D loads would.
-bool make_tmap_tiles128(CUtensorMap* map, const void* base, uint64_t rows, uint64_t planes) {
+bool make_tmap_tiles128(CUtensorMap* map, const void* base, uint64_t rows, uint64_t planes,
+                        uint32_t box_halves) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[4] = {64, rows, 2, planes};
   cuuint64_t strides[3] = {(cuuint64_t)kHeadDim * 2, 128, rows * kHeadDim * 2};
-  cuuint32_t box[4] = {64, 128, 2, 1};
+  cuuint32_t box[4] = {64, 128, box_halves, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -38,6 +38,18 @@ constexpr int kRing = 5;                      // shared K/V tile ring
 #define FPB_SCHED_SLEEP 256  // ns; measured: 128K -5.7%, 32K / 256K neutral (r1_ab_fa_sched_sleep)
 #endif
 constexpr float kRescaleThreshold = 8.0f;     // lazy O rescale (log2 units)
+// Timing probes (wrong numerics; tools/ab_probe.sh): 1 = softmax without max/exp2 (P = raw S),
+// 2 = exp2 replaced by one FMA (no MUFU), 3 = no MMA issued (barriers only), 4 = 1 + 3,
+// 5 = K/V tiles loaded as one 64-column half (half the L2 -> SMEM bytes), 6 = 4 without the
+// tcgen05.ld of S, 7 = 6 loading a quarter of S.
+#ifndef FPB_FA_PROBE
+#define FPB_FA_PROBE 0
+#endif
+#if FPB_FA_PROBE == 2
+#define FA_EX2(x) fmaf((x), 0.001f, 1.0f)
+#else
+#define FA_EX2(x) ex2_approx(x)
+#endif
 
 struct FaParams {
   Dims D;
@@ -269,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       TR_ADD(12);  // producer: waiting for a free ring slot
       if (lane == 0) {
         const uint32_t fb = smem_u32(&s.kv_full[r]);
-        mbar_arrive_expect_tx(fb, kTile);
+        mbar_arrive_expect_tx(fb, (FPB_FA_PROBE == 5 || FPB_FA_PROBE == 8) ? kTile / 2 : kTile);
         tma_load_4d_hint(smem_u32(s.ring[r]), map, fb, 0, row, 0, plane, pol_kv);  // whole tile
       }
       __syncwarp();
@@ -371,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(smem_u32(half ? &s.p_full[sl] : &s.p_half[sl]), (S.bc - 1) & 1);
             tc_fence_after();
             TR_ADD(9 + half);  // MMA: waiting for P half
-            if (leader) {
+            if (leader && FPB_FA_PROBE != 3 && FPB_FA_PROBE != 4 && FPB_FA_PROBE < 6) {
 #pragma unroll
               for (int k4 = 0; k4 < 4; ++k4) {
                 const int ks = half * 4 + k4;
@@ -401,7 +413,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
               const uint64_t off = ((ks >> 2) * (kTile / 2) + (ks & 3) * 32) >> 4;
-              mma_bf16_ss(s_tmem, qdesc + off, kdesc + off, idesc_qk, ks > 0 ? 1u : 0u);
+              if (FPB_FA_PROBE != 3 && FPB_FA_PROBE != 4 && FPB_FA_PROBE < 6)
+                mma_bf16_ss(s_tmem, qdesc + off, kdesc + off, idesc_qk, ks > 0 ? 1u : 0u);
             }
             mma_commit(smem_u32(&s.kv_empty[r]));
             mma_commit(smem_u32(&s.s_full[sl]));
@@ -479,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               // (profiles/r1_fa_trace.txt)
               float x0, x1;
               ffma2(x0, x1, __uint_as_float(v[c]), __uint_as_float(v[c + 1]), sc, sc, neg_m, neg_m);
-              const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
+              const float p0 = FA_EX2(x0), p1 = FA_EX2(x1);
               const int a = ((c >> 1) & 3) * 2;
               fadd2(bs[a], bs[a + 1], bs[a], bs[a + 1], p0, p1);
               v[c >> 1] = pack_bf16x2(p0, p1);
@@ -487,8 +500,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
 #pragma unroll
             for (int c = half * 64; c < half * 64 + 64; c += 2) {
-              const float p0 = ex2_approx(fmaf(__uint_as_float(v[c]), sc, neg_m));
-              const float p1 = ex2_approx(fmaf(__uint_as_float(v[c + 1]), sc, neg_m));
+              const float p0 = FA_EX2(fmaf(__uint_as_float(v[c]), sc, neg_m));
+              const float p1 = FA_EX2(fmaf(__uint_as_float(v[c + 1]), sc, neg_m));
               const int a = ((c >> 1) & 3) * 2;
               fadd2(bs[a], bs[a + 1], bs[a], bs[a + 1], p0, p1);
               v[c >> 1] = pack_bf16x2(p0, p1);
@@ -513,23 +526,40 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_used = m_new;
         };
         {
+#if FPB_FA_PROBE == 6 || FPB_FA_PROBE == 7
+#pragma unroll
+          for (int c = 0; c < 128; ++c) v[c] = (uint32_t)c;
+#if FPB_FA_PROBE == 7
+          tmem_ld32(s_addr + 0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));  // a quarter of S
+          tmem_ld_wait();
+#endif
+#else
           tmem_ld64(s_addr + 0, &v[0]);
           tmem_ld64(s_addr + 64, &v[64]);
           tmem_ld_wait();
+#endif
+#if FPB_FA_PROBE == 1 || FPB_FA_PROBE == 4 || FPB_FA_PROBE == 6 || FPB_FA_PROBE == 7 || FPB_FA_PROBE == 8
+          const float m_new = 0.f;
+#else
           mask_half(0);
           mask_half(1);
           const float m_new = fmaxf(m_used, fmaxf(max_half(0), max_half(1)) * sc);
+#endif
           TR_ADD(1);  // softmax: TMEM load + mask + row max
           if (n == 0)
             m_used = m_new;
           else if (__any_sync(0xffffffffu, m_new > m_used + kRescaleThreshold))
             rescale(m_new);
           TR_ADD(2);  // softmax: lazy O rescale (rare)
+#if FPB_FA_PROBE != 1 && FPB_FA_PROBE != 4 && FPB_FA_PROBE < 6
           exp_half(0, -m_used);
+#endif
         }
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
+#if FPB_FA_PROBE != 1 && FPB_FA_PROBE != 4 && FPB_FA_PROBE < 6
           if (half == 1) exp_half(1, -m_used);
+#endif
           tmem_st32(s_addr + half * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[half * 32]));
           tmem_st_wait();
           tc_fence_before();
@@ -632,8 +662,8 @@ cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __n
                                 int32_t* plan_error, int* sched, uint16_t* lists, cudaStream_t s) {
   CUtensorMap tm_q, tm_k, tm_v, tm_o;
   if (!make_tmap_tiles128(&tm_q, Q, D.L, (uint64_t)D.Z * D.Hq) ||
-      !make_tmap_tiles128(&tm_k, K, D.L, (uint64_t)D.Z * D.Hkv) ||
-      !make_tmap_tiles128(&tm_v, V, D.L, (uint64_t)D.Z * D.Hkv) ||
+      !make_tmap_tiles128(&tm_k, K, D.L, (uint64_t)D.Z * D.Hkv, (FPB_FA_PROBE == 5 || FPB_FA_PROBE == 8) ? 1 : 2) ||
+      !make_tmap_tiles128(&tm_v, V, D.L, (uint64_t)D.Z * D.Hkv, (FPB_FA_PROBE == 5 || FPB_FA_PROBE == 8) ? 1 : 2) ||
       !make_tmap_rows128(&tm_o, out_bf16 ? out : Q, D.L, (uint64_t)D.Z * D.Hq))
     return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(sched, 0, sizeof(int), s);

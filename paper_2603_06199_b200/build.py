@@ -7,7 +7,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["abi.cu", "pool.cu", "select.cu", "discover.cu", "attention.cu", "attention_fa.cu", "attention_fa2.cu",
+SOURCES = ["abi.cu", "pool.cu", "select.cu", "discover.cu", "attention.cu", "attention_fa.cu",
            "generic.cu", "baselines.cu"]
 HEADERS = ["fp_ptx.cuh", "fp_common.cuh", "fp_kernels.h"]
 LIB = os.path.join(HERE, "libfpb200.so")

@@ -367,15 +367,9 @@ cudaError_t launch_attention(const Dims& D, int splits, const __nv_bfloat16* Q,
                              const int32_t* counts, bool out_bf16, void* out, float* lse,
                              unsigned long long* visits, int32_t* plan_error, int* sched,
                              uint16_t* lists, cudaStream_t s) {
-  if (splits == 1) {
-    static const bool v1 = [] {
-      const char* e = std::getenv("FPB_FA_V1");  // A/B switch: the two-slot kernel
-      return e && e[0] == '1';
-    }();
-    return (v1 ? launch_attention_fa : launch_attention_fa2)(D, Q, K, V, idx, counts, out_bf16,
-                                                             out, lse, visits, plan_error, sched,
-                                                             lists, s);
-  }
+  if (splits == 1)
+    return launch_attention_fa(D, Q, K, V, idx, counts, out_bf16, out, lse, visits, plan_error,
+                               sched, lists, s);
   CUtensorMap tm_q, tm_k, tm_v;
   if (!make_tmap_rows128(&tm_q, Q, D.L, (uint64_t)splits * D.Z * D.Hq) ||
       !make_tmap_rows128(&tm_k, K, D.L, (uint64_t)splits * D.Z * D.Hkv) ||

@@ -67,11 +67,6 @@ cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __n
                                 const __nv_bfloat16* V, const int32_t* idx, const int32_t* counts,
                                 bool out_bf16, void* out, float* lse, unsigned long long* visits,
                                 int32_t* plan_error, int* sched, uint16_t* lists, cudaStream_t s);
-// attention_fa2.cu — one item per CTA, S double-buffered (the default bf16 kernel)
-cudaError_t launch_attention_fa2(const Dims& D, const __nv_bfloat16* Q, const __nv_bfloat16* K,
-                                 const __nv_bfloat16* V, const int32_t* idx, const int32_t* counts,
-                                 bool out_bf16, void* out, float* lse, unsigned long long* visits,
-                                 int32_t* plan_error, int* sched, uint16_t* lists, cudaStream_t s);
 // bytes of the compacted-plan scratch launch_attention needs (grid x 2 slots x 2 bufs x M x u16)
 size_t attention_list_bytes(const Dims& D);
 size_t attention_f32_smem_bytes(const Dims& D);  // fp32-input kernel (attention.cu)

@@ -186,7 +186,7 @@ size_t ws_attention(const Dims& D, fpb_dtype t) {
   return kSchedBytes + align_up(attention_list_bytes(D)) +
          (t == FPB_F32 ? align_up(2 * q_elems(D) * 2) + align_up(2 * kv_elems(D) * 2) +
                              align_up(kv_elems(D) * 2)
-                       : 0);
+                       : align_up(attention_phase_bytes(D)));
 }
 
 cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -578,12 +578,12 @@ static int attention_common(const fpb_problem* p, fpb_dtype dtype, const void* Q
     k = k2;
     v = v2;
   }
-FPB_CUDA(launch_attention(D, dtype == FPB_F32 ? 2 : 1, q, k, v, idx, counts,
+  uint8_t* wsb = static_cast<uint8_t*>(workspace);
+  FPB_CUDA(launch_attention(D, dtype == FPB_F32 ? 2 : 1, q, k, v, idx, counts,
                             out_dtype == FPB_BF16, out, lse, visits, plan_error,
-                            static_cast<int*>(workspace),
-                            reinterpret_cast<uint16_t*>(static_cast<uint8_t*>(workspace) +
-                                                        kSchedBytes),
-                            S(stream)));
+                            reinterpret_cast<int*>(wsb),
+                            reinterpret_cast<uint16_t*>(wsb + kSchedBytes),
+                            wsb + kSchedBytes + align_up(attention_list_bytes(D)), S(stream)));
   return FPB_OK;
 }
 

@@ -366,10 +366,10 @@ cudaError_t launch_attention(const Dims& D, int splits, const __nv_bfloat16* Q,
                              const __nv_bfloat16* K, const __nv_bfloat16* V, const int32_t* idx,
                              const int32_t* counts, bool out_bf16, void* out, float* lse,
                              unsigned long long* visits, int32_t* plan_error, int* sched,
-                             uint16_t* lists, cudaStream_t s) {
+                             uint16_t* lists, uint8_t* phase_ws, cudaStream_t s) {
   if (splits == 1)
     return launch_attention_fa(D, Q, K, V, idx, counts, out_bf16, out, lse, visits, plan_error,
-                               sched, lists, s);
+                               sched, lists, phase_ws, s);
   CUtensorMap tm_q, tm_k, tm_v;
   if (!make_tmap_rows128(&tm_q, Q, D.L, (uint64_t)splits * D.Z * D.Hq) ||
       !make_tmap_rows128(&tm_k, K, D.L, (uint64_t)splits * D.Z * D.Hkv) ||

@@ -38,6 +38,8 @@ constexpr int kRing = 5;                      // shared K/V tile ring
 #define FPB_SCHED_SLEEP 256  // ns; measured: 128K -5.7%, 32K / 256K neutral (r1_ab_fa_sched_sleep)
 #endif
 constexpr float kRescaleThreshold = 8.0f;     // lazy O rescale (log2 units)
+constexpr int kPartFloats = kBlock * kHeadDim + 2 * kBlock;  // one row's partial: O, m, l
+constexpr double kPhaseBytes = 64.0 * 1024 * 1024;  // K/V bytes of one KV-range phase (L2 budget)
 // Timing probes (wrong numerics; tools/ab_probe.sh): 1 = softmax without max/exp2 (P = raw S),
 // 2 = exp2 replaced by one FMA (no MUFU), 3 = no MMA issued (barriers only), 4 = 1 + 3,
 // 5 = K/V tiles loaded as one 64-column half (half the L2 -> SMEM bytes), 6 = 4 without the
@@ -64,6 +66,11 @@ struct FaParams {
   int num_items;
   int out_bf16;
   int gs;     // KV groups per super-group of the work order (divides Hkv)
+  // KV-range phases (fa_phases): one KV group's key blocks in `phases` ranges of `chunk` blocks,
+  // one launch per range (`phase`); stream order makes range p-1 complete before range p starts
+  int phases, chunk, phase;
+  float* part;   // partial (O, m, l) of rows that continue in a later phase
+  int* pflag;    // per (z, h, query block): 1 when the row's partial holds visited blocks
 };
 
 #ifdef FPB_TRACE
@@ -93,7 +100,11 @@ __device__ unsigned long long g_trace[16];
 struct SlotMeta {
   int item;  // -1: no more work
   int nblk;
+  int zh, qi, zkv;  // (z * Hq + h), query block, K/V plane
+  int jbase;        // first key block of the item's KV range (dense lists)
+  int mode;         // kContinue: O/m/l start from the row's partial; kPartialOut: write one
 };
+constexpr int kContinue = 1, kPartialOut = 2;
 
 struct FaSmem {
   uint8_t q[2][kTile];
@@ -122,6 +133,17 @@ __device__ __forceinline__ void decode(const Dims& D, int gs, int item, int& z, 
   z = t / nsg;
 }
 
+// A KV-range phase launch holds the rows qi >= phase * chunk of every (z, KV group): per (z, KV
+// group) heavy (long) rows first, the group's Q heads fastest.
+__device__ __forceinline__ void decode_phased(const Dims& D, int phase, int chunk, int item,
+                                              int& z, int& h, int& qi) {
+  const int per_zg = (D.M - phase * chunk) * D.group;
+  const int zg = item / per_zg, u = item % per_zg;
+  z = zg / D.Hkv;
+  h = (zg % D.Hkv) * D.group + u % D.group;
+  qi = D.M - 1 - u / D.group;
+}
+
 // Per-slot progress shared by the producer's and the MMA issuer's identical unit schedules.
 struct SlotState {
   int t = 0;      // items taken by this slot (incl. empty ones and the final sentinel)
@@ -130,6 +152,8 @@ struct SlotState {
   int item = 0;
   int qc = 0;     // items with nblk > 0 (Q loads / O lifetimes)
   int zkv = 0;    // K/V plane of the current item (producer)
+  int jbase = 0;  // first key block of the item's range (dense lists, producer)
+  bool cont = false;  // the item's O starts from a partial (issuer: accumulate from PV(0))
   int bc = 0;     // blocks processed (P / S / O barrier phases)
   bool active = true;
 };
@@ -206,11 +230,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= prm.num_items) item = -1;
         int nblk = 0;
+        SlotMeta mt{item, 0, 0, 0, 0, 0, 0};
         if (item >= 0) {
           int z, h, qi;
-          decode(D, prm.gs, item, z, h, qi);
+          const int ph = prm.phase;
+          if (prm.phases > 1)
+            decode_phased(D, ph, prm.chunk, item, z, h, qi);
+          else
+            decode(D, prm.gs, item, z, h, qi);
+          mt.zh = z * D.Hq + h;
+          mt.qi = qi;
+          mt.zkv = z * D.Hkv + h / D.group;
+          // this item's KV range: [lo, hi); a row's last phase also takes every listed block
+          // beyond its own range (listed j > i blocks, attended in full)
+          const int last_ph = prm.phases > 1 ? min(qi / prm.chunk, prm.phases - 1) : 0;
+          const int lo = ph * prm.chunk, hi = ph == last_ph ? N : lo + prm.chunk;
+          mt.jbase = lo;
+          if (ph < last_ph) mt.mode |= kPartialOut;
+          bool valid = false;  // the earlier phases visited blocks: a partial (O, m, l) exists
+          if (ph > 0) {
+            valid = __ldcg(prm.pflag + (size_t)mt.zh * D.M + qi) != 0;
+            if (valid) mt.mode |= kContinue;
+          }
           if (dense) {
-            nblk = qi + 1;
+            nblk = max(0, min(qi + 1, hi) - lo);
           } else {
             int C = prm.counts[((size_t)z * D.M + qi) * D.Hq + h];
             if (C > N) {  // a row has N slots: more is a malformed plan, never read past it
@@ -225,42 +268,49 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (slot < C) bid = prm.idx[(prow + slot) * D.Hq + h];
               const bool ok = slot < C && bid >= 0 && bid < N;
               if (slot < C && !ok && prm.plan_error) atomicExch(prm.plan_error, 1);
-              const unsigned bal = __ballot_sync(0xffffffffu, ok);
-              if (ok) lst[nblk + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)bid;
+              const bool mine = ok && bid >= lo && bid < hi;
+              const unsigned bal = __ballot_sync(0xffffffffu, mine);
+              if (mine) lst[nblk + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)bid;
               nblk += __popc(bal);
             }
             if (lane == 0 && prm.visits && nblk) atomicAdd(prm.visits, (unsigned long long)nblk);
-            if (nblk == 0) {
-              // C = 0 (or only out-of-range slots): out = 0 * (1/0) = NaN, lse = -inf
-              // (attention.hpp:121-125), written here.  An empty item never reaches the other
-              // roles: its softmax warps would release the meta / list buffer before the producer
-              // and the MMA issuer had read it.
+          }
+          if (nblk == 0) {
+            // Nothing to attend in this range.  An empty item never reaches the other roles
+            // (its softmax warps would release the meta / list buffer before the producer and
+            // the MMA issuer had read it): the scheduler settles it here.
+            if (mt.mode & kPartialOut) {
+              // the row goes on: its partial state (or its absence) passes along unchanged
+            } else {
+              // final: out = O / l and lse = m + log2 l from the partial, or, with no block
+              // visited at all (C = 0), out = 0 * (1/0) = NaN, lse = -inf (attention.hpp:121-125)
               const int rows = block_len(D, qi);
-              const size_t orow0 = ((size_t)z * D.Hq + h) * (size_t)D.L + (size_t)qi * kBlock;
-              const float nan = __int_as_float(0x7fc00000);
-              const int vec_per_row = prm.out_bf16 ? kHeadDim / 8 : kHeadDim / 4;
-              for (int e = lane; e < rows * vec_per_row; e += 32) {
-                const size_t row = orow0 + e / vec_per_row;
-                const int v4 = e % vec_per_row;
-                if (prm.out_bf16) {
-                  const uint32_t pn = pack_bf16x2(nan, nan);
-                  reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(prm.out) +
-                                           row * kHeadDim)[v4] = make_uint4(pn, pn, pn, pn);
-                } else {
-                  reinterpret_cast<float4*>(reinterpret_cast<float*>(prm.out) +
-                                            row * kHeadDim)[v4] = make_float4(nan, nan, nan, nan);
-                }
+              const size_t orow0 = (size_t)mt.zh * D.L + (size_t)qi * kBlock;
+              const size_t ps = valid ? (size_t)mt.zh * (D.M - prm.chunk) + (qi - prm.chunk) : 0;
+              const float* po = prm.part + ps * (kBlock * kHeadDim + 2 * kBlock);
+              const float* pml = po + kBlock * kHeadDim;
+              for (int e = lane; e < rows * kHeadDim; e += 32) {
+                const int rr = e / kHeadDim;  // out = O * (1 / l), as in the epilogue
+                const float val = valid ? __ldcg(po + e) * (1.0f / __ldcg(pml + kBlock + rr))
+                                        : __int_as_float(0x7fc00000);
+                if (prm.out_bf16)
+                  reinterpret_cast<__nv_bfloat16*>(prm.out)[orow0 * kHeadDim + e] =
+                      __float2bfloat16_rn(val);
+                else
+                  reinterpret_cast<float*>(prm.out)[orow0 * kHeadDim + e] = val;
               }
-              for (int r = lane; r < rows; r += 32) prm.lse[orow0 + r] = -INFINITY;
-              __syncwarp();
-              continue;  // fetch another item for this slot; nothing is published
+              for (int rr = lane; rr < rows; rr += 32)
+                prm.lse[orow0 + rr] =
+                    valid ? __ldcg(pml + rr) + log2f(__ldcg(pml + kBlock + rr)) : -INFINITY;
             }
+            __syncwarp();
+            continue;  // fetch another item for this slot; nothing is published
           }
         }
+        mt.nblk = nblk;
         __syncwarp();
         if (lane == 0) {
-          s.meta[sl][p].item = item;
-          s.meta[sl][p].nblk = nblk;
+          s.meta[sl][p] = mt;
           mbar_arrive(smem_u32(&s.meta_full[sl][p]));
         }
         __syncwarp();
@@ -298,19 +348,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(smem_u32(&s.meta_full[sl][p]), (S.t >> 1) & 1);
             TR_ADD(14);  // producer: waiting for the scheduler
           }
-          S.item = s.meta[sl][p].item;
-          S.nblk = s.meta[sl][p].nblk;
+          const SlotMeta mt = s.meta[sl][p];
+          S.item = mt.item;
+          S.nblk = mt.nblk;
           if (S.item < 0) {
             S.active = false;
             continue;
           }
-          if (S.nblk == 0) {  // nothing to load; the softmax warps write NaN / -inf
-            ++S.t;
-            continue;
-          }
-          int z, h, qi;
-          decode(D, prm.gs, S.item, z, h, qi);
-          S.zkv = z * D.Hkv + h / D.group;
+          S.zkv = mt.zkv;
+          S.jbase = mt.jbase;
           {
             TR_T0();
             if (S.qc >= 1) mbar_wait(smem_u32(&s.q_empty[sl]), (S.qc - 1) & 1);
@@ -319,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) {
             const uint32_t qb = smem_u32(&s.q_full[sl]);
             mbar_arrive_expect_tx(qb, kTile);
-            tma_load_4d_hint(smem_u32(s.q[sl]), &tm_q, qb, 0, qi * kBlock, 0, z * D.Hq + h, pol_q);
+            tma_load_4d_hint(smem_u32(s.q[sl]), &tm_q, qb, 0, mt.qi * kBlock, 0, mt.zh, pol_q);
           }
           __syncwarp();
           ++S.qc;
@@ -327,8 +373,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- one unit: V(j-1) then K(j), matching the MMA issue order PV(j-1), QK(j)
         const int zkv = S.zkv;
         const uint16_t* lst = list_of(sl, p);
-        if (S.j >= 1) push(&tm_v, (dense ? S.j - 1 : (int)lst[S.j - 1]) * kBlock, zkv);
-        if (S.j < S.nblk) push(&tm_k, (dense ? S.j : (int)lst[S.j]) * kBlock, zkv);
+        if (S.j >= 1) push(&tm_v, (dense ? S.jbase + S.j - 1 : (int)lst[S.j - 1]) * kBlock, zkv);
+        if (S.j < S.nblk) push(&tm_k, (dense ? S.jbase + S.j : (int)lst[S.j]) * kBlock, zkv);
         if (++S.j == S.nblk + 1) {
           S.j = 0;
           ++S.t;
@@ -352,12 +398,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(smem_u32(&s.meta_full[sl][p]), (S.t >> 1) & 1);
           S.item = s.meta[sl][p].item;
           S.nblk = s.meta[sl][p].nblk;
+          S.cont = (s.meta[sl][p].mode & kContinue) != 0;
           if (S.item < 0) {
             S.active = false;
-            continue;
-          }
-          if (S.nblk == 0) {
-            ++S.t;
             continue;
           }
           {
@@ -388,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int k4 = 0; k4 < 4; ++k4) {
                 const int ks = half * 4 + k4;
                 mma_bf16_ts(o_tmem, s_tmem + ks * 8, vdesc + (uint64_t)(ks * 2048 >> 4), idesc_pv,
-                            (m > 0 || ks > 0) ? 1u : 0u);
+                            (m > 0 || ks > 0 || S.cont) ? 1u : 0u);
               }
             }
             __syncwarp();
@@ -443,16 +486,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = 0;; ++t) {
       const int p = t & 1;
       mbar_wait(smem_u32(&s.meta_full[sl][p]), (t >> 1) & 1);
-      const int item = s.meta[sl][p].item;
-      const int nblk = s.meta[sl][p].nblk;
-      if (item < 0) break;
+      const SlotMeta mt = s.meta[sl][p];
+      if (mt.item < 0) break;
+      const int nblk = mt.nblk, qi = mt.qi, zh = mt.zh;
+      const bool cont = (mt.mode & kContinue) != 0;
       const uint16_t* lst = list_of(sl, p);
-      int z, h, qi;
-      decode(D, prm.gs, item, z, h, qi);
       const int rows = block_len(D, qi);
       float m_used = -INFINITY, l = 0.f;
+      // rows that span several KV-range phases carry (O, m, l) between them (fa_phases)
+      float* po = nullptr;
+      if (mt.mode & (kContinue | kPartialOut))
+        po = prm.part + ((size_t)zh * (D.M - prm.chunk) + (qi - prm.chunk)) * kPartFloats;
+      if (cont) {  // O starts from the partial (the slot's previous O was read out above)
+        m_used = __ldcg(po + kBlock * kHeadDim + r);
+        l = __ldcg(po + kBlock * kHeadDim + kBlock + r);
+        const float4* src = reinterpret_cast<const float4*>(po + (size_t)r * kHeadDim);
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t o[32];
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const float4 x = __ldcs(src + cc * 8 + q4);  // read once: evict first
+            o[4 * q4] = __float_as_uint(x.x);
+            o[4 * q4 + 1] = __float_as_uint(x.y);
+            o[4 * q4 + 2] = __float_as_uint(x.z);
+            o[4 * q4 + 3] = __float_as_uint(x.w);
+          }
+          tmem_st32(o_addr + cc * 32, o);
+        }
+        tmem_st_wait();
+      }
       for (int n = 0; n < nblk; ++n, ++bc) {
-        const int kv = dense ? n : (int)lst[n];
+        const int kv = dense ? mt.jbase + n : (int)lst[n];
         const int cols = block_len(D, kv);
         const int lim = (kv == qi) ? min(cols, r + 1) : cols;  // attention.hpp:85-91
         const bool full = __all_sync(0xffffffffu, lim == kBlock);
@@ -546,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float m_new = fmaxf(m_used, fmaxf(max_half(0), max_half(1)) * sc);
 #endif
           TR_ADD(1);  // softmax: TMEM load + mask + row max
-          if (n == 0)
+          if (n == 0 && !cont)
             m_used = m_new;
           else if (__any_sync(0xffffffffu, m_new > m_used + kRescaleThreshold))
             rescale(m_new);
@@ -571,8 +636,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       TR_T0();
       // ---- epilogue (attention.hpp:119-126)
-      const size_t orow = ((size_t)z * D.Hq + h) * (size_t)D.L + (size_t)qi * kBlock + r;
-      if (nblk > 0) {
+      const size_t orow = (size_t)zh * D.L + (size_t)qi * kBlock + r;
+      if (mt.mode & kPartialOut) {
+        // the row continues in a later KV-range phase: hand over O (unnormalised), m and l
+        mbar_wait(smem_u32(&s.o_done[sl]), (bc - 1) & 1);
+        tc_fence_after();
+        float4* dst = reinterpret_cast<float4*>(po + (size_t)r * kHeadDim);
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t o[32];
+          tmem_ld32(o_addr + cc * 32, o);
+          tmem_ld_wait();
+          if (cc == 3) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&s.o_free[sl]));
+          }
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4)
+            __stcs(dst + cc * 8 + q4,  // streamed (re-read only by the next phase's launch)
+                   make_float4(__uint_as_float(o[4 * q4]), __uint_as_float(o[4 * q4 + 1]),
+                               __uint_as_float(o[4 * q4 + 2]), __uint_as_float(o[4 * q4 + 3])));
+        }
+        __stcg(po + kBlock * kHeadDim + r, m_used);
+        __stcg(po + kBlock * kHeadDim + kBlock + r, l);
+        named_bar_sync(1 + sl, 128);
+        if (r == 0) {
+          prm.pflag[(size_t)zh * D.M + qi] = 1;  // read by the next phase's launch
+          mbar_arrive(smem_u32(&s.q_empty[sl]));
+        }
+        ++qc;
+      } else if (nblk > 0) {
         mbar_wait(smem_u32(&s.o_done[sl]), (bc - 1) & 1);  // last PV done => last QK done too
         tc_fence_after();
         const float inv = 1.0f / l;
@@ -619,8 +713,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_proxy_async_smem();
           named_bar_sync(1 + sl, 128);
           if (r == 0) {  // rows beyond L are clipped by the tensor map
-            tma_store_3d(&tm_o, stage, 0, qi * kBlock, z * D.Hq + h);
-            tma_store_3d(&tm_o, stage + kTile / 2, 64, qi * kBlock, z * D.Hq + h);
+            // O is written once and never re-read here: keep it from evicting K/V lines
+            const uint64_t pol_o = policy_evict_first();
+            tma_store_3d_hint(&tm_o, stage, 0, qi * kBlock, zh, pol_o);
+            tma_store_3d_hint(&tm_o, stage + kTile / 2, 64, qi * kBlock, zh, pol_o);
             bulk_commit();
             bulk_wait_read0();
             mbar_arrive(smem_u32(&s.q_empty[sl]));
@@ -656,10 +752,44 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
+// KV-range phases: when one KV group's K and V exceed the L2 budget (kPhaseBytes), its key blocks
+// are processed in `phases` ranges of `chunk` blocks, one launch per range; within a launch the
+// work order is still KV-group-major, so all Q heads of a group stream the same L2-sized slice of
+// its K/V (at 256K one Qwen3 group's K/V is 128 MB, above the 126 MB L2).  Rows
+// spanning several ranges carry their exact fp32 (O, m, l) through a global partial buffer, so the
+// arithmetic, and the result, equal the single-launch kernel's bit for bit.  Whole-row problems
+// only (no row shards); FPB_FA_PHASES overrides (measurement switch).
+int fa_phases(const Dims& D, int* chunk) {
+  static const int env = [] {
+    const char* e = std::getenv("FPB_FA_PHASES");
+    return e ? std::atoi(e) : 0;
+  }();
+  int P = 1;
+  if (D.rs == 1 && !D.zz && D.Mr == D.M) {
+    const double group_bytes = 2.0 * D.L * D.d * 2.0;
+    P = env > 0 ? env : (int)((group_bytes + kPhaseBytes - 1) / kPhaseBytes);
+    P = P < 1 ? 1 : (P > 8 ? 8 : P);
+  }
+  int c = (D.M + P - 1) / P;
+  if (P > 1 && c < 4) P = 1;  // not worth it for a few key blocks
+  if (P == 1) c = D.M;
+  P = (D.M + c - 1) / c;
+  if (chunk) *chunk = c;
+  return P;
+}
+
+size_t attention_phase_bytes(const Dims& D) {
+  int c;
+  if (fa_phases(D, &c) == 1) return 0;
+  const size_t flags = ((size_t)D.Z * D.Hq * D.M * sizeof(int) + 1023) / 1024 * 1024;
+  return flags + (size_t)D.Z * D.Hq * (D.M - c) * kPartFloats * sizeof(float);
+}
+
 cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __nv_bfloat16* K,
                                 const __nv_bfloat16* V, const int32_t* idx, const int32_t* counts,
                                 bool out_bf16, void* out, float* lse, unsigned long long* visits,
-                                int32_t* plan_error, int* sched, uint16_t* lists, cudaStream_t s) {
+                                int32_t* plan_error, int* sched, uint16_t* lists,
+                                uint8_t* phase_ws, cudaStream_t s) {
   CUtensorMap tm_q, tm_k, tm_v, tm_o;
   if (!make_tmap_tiles128(&tm_q, Q, D.L, (uint64_t)D.Z * D.Hq) ||
       !make_tmap_tiles128(&tm_k, K, D.L, (uint64_t)D.Z * D.Hkv, (FPB_FA_PROBE == 5 || FPB_FA_PROBE == 8) ? 1 : 2) ||
@@ -671,8 +801,18 @@ cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __n
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int num_items = D.Z * D.Hq * D.Mr;
-  const int grid = num_items < sms ? num_items : sms;
+  int chunk = D.M;
+  const int phases = fa_phases(D, &chunk);
+  int* pflag = nullptr;
+  float* part = nullptr;
+  if (phases > 1) {
+    if (!phase_ws) return cudaErrorInvalidValue;
+    pflag = reinterpret_cast<int*>(phase_ws);
+    part = reinterpret_cast<float*>(
+        phase_ws + ((size_t)D.Z * D.Hq * D.M * sizeof(int) + 1023) / 1024 * 1024);
+    e = cudaMemsetAsync(pflag, 0, (size_t)D.Z * D.Hq * D.M * sizeof(int), s);
+    if (e != cudaSuccess) return e;
+  }
   // K/V bytes of one KV group = 2 tensors x L x d x 2 B; keep gs groups' worth <= 64 MiB
   // (measured: 32K prefers all 4 Qwen3 groups interleaved, 128K/256K one group at a time).
   // FPB_FA_GS overrides (measurement switch).
@@ -683,17 +823,28 @@ cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __n
   int gs = gs_env;
   if (gs <= 0) {
     const double group_bytes = 2.0 * D.L * D.d * 2.0;
-    gs = (int)((64.0 * 1024 * 1024) / group_bytes);
+    gs = (int)(kPhaseBytes / group_bytes);
   }
   gs = gs < 1 ? 1 : (gs > D.Hkv ? D.Hkv : gs);
   while (D.Hkv % gs) --gs;
-  FaParams prm{D, idx, counts, out, lse, visits, plan_error, sched, lists, num_items,
-               out_bf16 ? 1 : 0, gs};
+  if (phases > 1) gs = 1;
   const size_t smem = sizeof(FaSmem) + 1024;
   e = cudaFuncSetAttribute(fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  fa_kernel<<<grid, kThreads, smem, s>>>(tm_q, tm_k, tm_v, tm_o, prm);
-  return cudaGetLastError();
+  for (int ph = 0; ph < phases; ++ph) {
+    const int num_items = phases > 1 ? D.Z * D.Hq * (D.M - ph * chunk) : D.Z * D.Hq * D.Mr;
+    if (ph > 0) {  // the next launch restarts the work counter
+      e = cudaMemsetAsync(sched, 0, sizeof(int), s);
+      if (e != cudaSuccess) return e;
+    }
+    const int grid = num_items < sms ? num_items : sms;
+    FaParams prm{D,     idx,   counts, out,   lse,    visits, plan_error, sched,
+                 lists, num_items, out_bf16 ? 1 : 0, gs, phases, chunk, ph, part, pflag};
+    fa_kernel<<<grid, kThreads, smem, s>>>(tm_q, tm_k, tm_v, tm_o, prm);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace fpb

@@ -62,11 +62,15 @@ cudaError_t launch_attention(const Dims& D, int splits, const __nv_bfloat16* Q,
                              const __nv_bfloat16* K, const __nv_bfloat16* V, const int32_t* idx,
                              const int32_t* counts, bool out_bf16, void* out, float* lse,
                              unsigned long long* visits, int32_t* plan_error, int* sched,
-                             uint16_t* lists, cudaStream_t s);
+                             uint16_t* lists, uint8_t* phase_ws, cudaStream_t s);
 cudaError_t launch_attention_fa(const Dims& D, const __nv_bfloat16* Q, const __nv_bfloat16* K,
                                 const __nv_bfloat16* V, const int32_t* idx, const int32_t* counts,
                                 bool out_bf16, void* out, float* lse, unsigned long long* visits,
-                                int32_t* plan_error, int* sched, uint16_t* lists, cudaStream_t s);
+                                int32_t* plan_error, int* sched, uint16_t* lists,
+                                uint8_t* phase_ws, cudaStream_t s);
+// KV-range phases of the bf16 attention kernel (1 = none) and their workspace (flags + partials)
+int fa_phases(const Dims& D, int* chunk);
+size_t attention_phase_bytes(const Dims& D);
 // bytes of the compacted-plan scratch launch_attention needs (grid x 2 slots x 2 bufs x M x u16)
 size_t attention_list_bytes(const Dims& D);
 size_t attention_f32_smem_bytes(const Dims& D);  // fp32-input kernel (attention.cu)

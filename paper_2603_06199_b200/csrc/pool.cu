@@ -1,80 +1,67 @@
 // pool.cu — K1: block-mean key pooling (discovery.hpp:39-70) and operand conversions.
 //
-// HBM-bound.  One 64-thread CTA owns one (kv head, key block); each thread owns 2 channels and
-// sums the block's rows sequentially in fp32 — the reference's order (discovery.hpp:51-53) — then
-// multiplies by the fp32 reciprocal 1/len (discovery.hpp:55-56), so `pooled` is bit-identical to
-// the reference for identical inputs.  The same pass writes the bf16 hi/lo split of k̄ that the
-// tensor-core discovery kernel consumes (k̄ = hi + lo to 16 significant bits).
+// HBM-bound.  One CTA per (kv head, key block): a single bulk copy (cp.async.bulk, TMA engine)
+// stages the block's rows — contiguous in K (Z x Hkv x L x d) — in shared memory, 32 KiB for
+// bf16; one thread per channel then sums the rows sequentially in fp32, the reference's order
+// (discovery.hpp:51-53), and multiplies by the fp32 reciprocal 1/len (discovery.hpp:55-56), so
+// `pooled` is bit-identical to the reference for identical inputs.  With every block's copy in
+// flight at once (one wave: 7 CTAs of 32 KiB per SM) the kernel streams K at HBM rate.  The same
+// pass writes the bf16 hi/lo split of k̄ that the tensor-core discovery kernel consumes
+// (k̄ = hi + lo to 16 significant bits).
 #include <cuda_bf16.h>
+
+#include <type_traits>
 
 #include "fp_kernels.h"
 
 namespace fpb {
 
+using namespace ptx;
+
+__device__ __forceinline__ void bulk_load_1d(uint32_t dst, const void* src, uint32_t bytes,
+                                             uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
 template <bool kBf16>
-__global__ void __launch_bounds__(64) pool_keys_kernel(const void* __restrict__ K,
-                                                       float* __restrict__ pooled,
-                                                       __nv_bfloat16* __restrict__ split, int ZH,
-                                                       int L, int M, int last_len, int j0, int nj) {
-  // one CTA of 64 threads per (zh, key block j in [j0, j0 + nj)); thread t owns channels 2t, 2t+1
+__global__ void __launch_bounds__(kHeadDim) pool_keys_kernel(const void* __restrict__ K,
+                                                             float* __restrict__ pooled,
+                                                             __nv_bfloat16* __restrict__ split,
+                                                             int ZH, int L, int M, int last_len,
+                                                             int j0, int nj) {
+  using T = typename std::conditional<kBf16, __nv_bfloat16, float>::type;
+  extern __shared__ __align__(128) uint8_t tile_raw[];
+  const T* tile = reinterpret_cast<const T*>(tile_raw);
+  __shared__ uint64_t bar;
   const int zh = blockIdx.x / nj, j = j0 + blockIdx.x % nj;
-  const int c0 = threadIdx.x * 2;
   const int len = (j + 1 == M) ? last_len : kBlock;
   const size_t row0 = (size_t)zh * L + (size_t)j * kBlock;
-  float s0 = 0.f, s1 = 0.f;
-  constexpr int U = 16;  // independent row loads in flight; the add chain stays sequential in r
-  int r = 0;
-  for (; r + U <= len; r += U) {
-    float v[U][2];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const size_t off = (row0 + r + u) * kHeadDim + c0;
-      if constexpr (kBf16) {
-        const uint32_t raw = __ldg(reinterpret_cast<const unsigned int*>(
-            reinterpret_cast<const __nv_bfloat16*>(K) + off));
-        const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&raw);
-        v[u][0] = __low2float(a);
-        v[u][1] = __high2float(a);
-      } else {
-        const float2 f = __ldg(reinterpret_cast<const float2*>(reinterpret_cast<const float*>(K) + off));
-        v[u][0] = f.x;
-        v[u][1] = f.y;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {  // discovery.hpp:51-53: out[c] += row[c], r ascending
-      s0 = __fadd_rn(s0, v[u][0]);
-      s1 = __fadd_rn(s1, v[u][1]);
-    }
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1);
+    fence_mbar_init();
   }
-  for (; r < len; ++r) {
-    const size_t off = (row0 + r) * kHeadDim + c0;
-    float v0, v1;
-    if constexpr (kBf16) {
-      const __nv_bfloat16* p = reinterpret_cast<const __nv_bfloat16*>(K) + off;
-      v0 = __bfloat162float(p[0]);
-      v1 = __bfloat162float(p[1]);
-    } else {
-      const float* p = reinterpret_cast<const float*>(K) + off;
-      v0 = p[0];
-      v1 = p[1];
-    }
-    s0 = __fadd_rn(s0, v0);
-    s1 = __fadd_rn(s1, v1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = (uint32_t)(len * kHeadDim * sizeof(T));
+    mbar_arrive_expect_tx(smem_u32(&bar), bytes);
+    bulk_load_1d(smem_u32(tile_raw), reinterpret_cast<const T*>(K) + row0 * kHeadDim, bytes,
+                 smem_u32(&bar));
   }
-  const float inv = __fdiv_rn(1.0f, (float)len);  // discovery.hpp:55-56
-  const float o0 = __fmul_rn(s0, inv), o1 = __fmul_rn(s1, inv);
-  const size_t dst = ((size_t)zh * M + j) * kHeadDim + c0;
-  if (pooled) *reinterpret_cast<float2*>(pooled + dst) = make_float2(o0, o1);
+  mbar_wait(smem_u32(&bar), 0);
+  const int c = threadIdx.x;  // one channel per thread
+  float sum = 0.f;
+  for (int r = 0; r < len; ++r)  // discovery.hpp:51-53: out[c] += row[c], r ascending
+    sum = __fadd_rn(sum, static_cast<float>(tile[r * kHeadDim + c]));
+  const float o = __fmul_rn(sum, __fdiv_rn(1.0f, (float)len));  // discovery.hpp:55-56
+  const size_t dst = ((size_t)zh * M + j) * kHeadDim + c;
+  if (pooled) pooled[dst] = o;
   if (split) {
-    const __nv_bfloat16 h0 = __float2bfloat16_rn(o0), h1 = __float2bfloat16_rn(o1);
-    const __nv_bfloat162 hi = __halves2bfloat162(h0, h1);
-    const __nv_bfloat162 lo = __halves2bfloat162(
-        __float2bfloat16_rn(__fsub_rn(o0, __bfloat162float(h0))),
-        __float2bfloat16_rn(__fsub_rn(o1, __bfloat162float(h1))));
-    const size_t plane = (size_t)ZH * M * kHeadDim;
-    *reinterpret_cast<__nv_bfloat162*>(split + dst) = hi;
-    *reinterpret_cast<__nv_bfloat162*>(split + plane + dst) = lo;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(o);
+    split[dst] = hi;
+    split[(size_t)ZH * M * kHeadDim + dst] = __float2bfloat16_rn(__fsub_rn(o, __bfloat162float(hi)));
   }
 }
 
@@ -84,12 +71,17 @@ cudaError_t launch_pool_keys(const Dims& D, bool bf16_in, const void* K, float* 
   if (nj < 0) nj = D.M - j0;
   if (nj <= 0) return cudaSuccess;
   const dim3 grid(ZH * nj);
-  if (bf16_in)
-    pool_keys_kernel<true><<<grid, 64, 0, s>>>(K, pooled, kbar_split, ZH, D.L, D.M, D.last_len,
-                                               j0, nj);
-  else
-    pool_keys_kernel<false><<<grid, 64, 0, s>>>(K, pooled, kbar_split, ZH, D.L, D.M, D.last_len,
-                                                j0, nj);
+  if (bf16_in) {
+    pool_keys_kernel<true><<<grid, kHeadDim, kBlock * kHeadDim * 2, s>>>(
+        K, pooled, kbar_split, ZH, D.L, D.M, D.last_len, j0, nj);
+  } else {
+    constexpr int smem = kBlock * kHeadDim * 4;  // 64 KiB of fp32 rows
+    cudaError_t e = cudaFuncSetAttribute(pool_keys_kernel<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    pool_keys_kernel<false><<<grid, kHeadDim, smem, s>>>(K, pooled, kbar_split, ZH, D.L, D.M,
+                                                         D.last_len, j0, nj);
+  }
   return cudaGetLastError();
 }
 

@@ -512,7 +512,7 @@ def run_gpu_arm(args, rank, world, dist):
                      "sustained_note": "sustained peak = cuBLAS back to back under the 1000 W "
                                        "power cap (1335 MHz median), not this step's regime",
                      "traffic": ncu_traffic("fa_kernel", traffic_cfg),
-                     "traffic_unit": "bytes per launch (ncu --set full, cold L2)",
+                     "traffic_unit": "DRAM bytes per step of this kernel (ncu --set full, cold L2; summed over its launches: one per KV-range phase)",
                      "kernel": "fa_kernel (K4, csrc/attention_fa.cu)"
                                + (" on rank 0's shard" if world > 1 else "")},
         "discovery_roofline": {"bound": "hbm", "kernel": "pool_keys + discover_kernel + select",

@@ -73,29 +73,34 @@ _SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 
 def traffic(path, kernel, cfg):
+    """DRAM bytes (read + write) of one step's launches of `kernel` in the report, summed (the
+    attention kernel runs one launch per KV-range phase), filed under `cfg`."""
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
+    tot, n = 0.0, 0
     for r in rows[2:]:
         if kernel not in r[hdr.index("Kernel Name")]:
             continue
-        tot = 0.0
+        n += 1
         for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             i = hdr.index(key)
             tot += float(r[i].replace(",", "")) * _SCALE[units[i]]
-        dest = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                            "profiles", "ncu_traffic.json")
-        data = json.load(open(dest)) if os.path.exists(dest) else {}
-        recs = data.get(kernel, [])
-        recs = recs if isinstance(recs, list) else [recs]
-        recs = [x for x in recs if x.get("config") != cfg]  # one record per config
-        recs.append({"dram_bytes": tot, "config": cfg, "capture": os.path.basename(path)})
-        data[kernel] = recs
-        with open(dest, "w") as f:
-            json.dump(data, f, indent=1)
-        return tot
-    raise SystemExit(f"{kernel} not in {path}")
+    if not n:
+        raise SystemExit(f"{kernel} not in {path}")
+    dest = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "profiles", "ncu_traffic.json")
+    data = json.load(open(dest)) if os.path.exists(dest) else {}
+    recs = data.get(kernel, [])
+    recs = recs if isinstance(recs, list) else [recs]
+    recs = [x for x in recs if x.get("config") != cfg]  # one record per config
+    recs.append({"dram_bytes": tot, "launches": n, "config": cfg,
+                 "capture": os.path.basename(path)})
+    data[kernel] = recs
+    with open(dest, "w") as f:
+        json.dump(data, f, indent=1)
+    return tot
 
 
 if __name__ == "__main__":

@@ -50,6 +50,9 @@ constexpr uint32_t kEpiBar = 1;               // named barriers 1, 2: the two ep
 #define FPB_DISC_PRODUCER_WARP 2
 #endif
 constexpr uint32_t kMmaWarp = FPB_DISC_MMA_WARP;
+#ifndef FPB_DISC_M64
+#define FPB_DISC_M64 1
+#endif
 constexpr uint32_t kProducerWarp = FPB_DISC_PRODUCER_WARP;
 
 struct DiscParams {
@@ -72,6 +75,7 @@ struct DiscSmem {
   uint64_t it_full[kItemRing], it_empty[kItemRing];
   int items[kItemRing];
   int nch[kItemRing];  // k̄ chunks of the item (I / 128 + 1), decoded once by the producer
+  int lastlive[kItemRing];  // causal key blocks of its last chunk (I % 128 + 1)
   uint32_t tmem_base;
   float red[2][3][4];
   // followed by float m_s[M], S_s[M] per epilogue warpgroup, then int counts[ceil(M/128)][4]
@@ -169,6 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (item >= 0) {
           decode_item(D, item, z, h, I);
           s.nch[slot] = I / kBlock + 1;
+          s.lastlive[slot] = I % kBlock + 1;
         }
         s.items[slot] = item;
         mbar_arrive(smem_u32(&s.it_full[slot]));
@@ -208,7 +213,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer (one thread)
     if (elect_one()) {
-      constexpr uint32_t idesc = idesc_bf16_f32(128, 128, false, false);
+      constexpr uint32_t idesc128 = idesc_bf16_f32(128, 128, false, false);
+      // a last chunk with at most 64 causal key blocks: an M = 64 MMA on its first 64 k̄ rows
+      // (half the tensor work; the accumulator rows land in lanes 0-15 of each TMEM quarter)
+      constexpr uint32_t idesc64 = idesc_bf16_f32(64, 128, false, false);
       int gc = 0, dc0 = 0, dc1 = 0;  // chunks issued in total / per epilogue warpgroup
       for (int t = 0;; ++t) {
         const int slot = t % kItemRing;
@@ -217,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         DT_ADD(19);  // MMA: waiting for the next item
         const int item = s.items[slot];
         const int nchunks = s.nch[slot];
+        const int lastlive = s.lastlive[slot];
         mbar_arrive(smem_u32(&s.it_empty[slot]));
         if (item < 0) break;
         const int qb = t % kQBuf, wg = t & 1;
@@ -238,6 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t a_lo = sdesc_sw128(smem_u32(s.kb[st][1]), 16, 1024);
           const uint64_t b_q0 = sdesc_sw128(smem_u32(s.q[qb][0]), 16, 1024);
           const uint64_t b_q1 = sdesc_sw128(smem_u32(s.q[qb][NQ - 1]), 16, 1024);
+          const uint32_t idesc =
+              (FPB_DISC_M64 && c == nchunks - 1 && lastlive <= 64) ? idesc64 : idesc128;
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {
             const uint64_t off = ((ks >> 2) * (kTile / 2) + (ks & 3) * 32) >> 4;
@@ -296,8 +307,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(smem_u32(&s.d_full[buf]), (dc >> 1) & 1);
         DT_ADD(0);  // epilogue: waiting for the accumulator
         tc_fence_after();
-        const int J = c * kBlock + et;
-        const bool warp_live = c * kBlock + w4 * 32 <= I;  // warp-uniform
+        // M = 64 last chunks (see the MMA issuer): key block 16 q + i sits in lane i < 16 of
+        // TMEM quarter q; lanes 16-31 hold nothing (J past the row)
+        const bool m64 = FPB_DISC_M64 && c == nchunks - 1 && (I % kBlock) < 64;
+        const int jl = m64 ? (lane < 16 ? w4 * 16 + (int)lane : kBlock) : et;
+        const int J = c * kBlock + jl;
+        const bool warp_live = c * kBlock + w4 * (m64 ? 16 : 32) <= I;  // warp-uniform
         float m = kNegSentinel, S = 0.f;
         if (warp_live) {
           uint32_t v[128];

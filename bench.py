@@ -157,8 +157,11 @@ def bench_config(args, world):
     return {"workload": f"Qwen3-30B-A3B attention layer (Hq={args.hq}, Hkv={args.hkv}, d=128) "
                         f"bf16 causal L={args.L}, alpha={args.alpha}, B=128, sink 256, window 512",
             "global_batch_sequences": 1, "seq_len": args.L,
-            "parallelism": (f"one layer split over {world} GPU(s): {part}; NCCL all-gather of "
-                            f"O + LSE inside the timed step" if world > 1 else "1 GPU"),
+            "parallelism": (f"one layer split over {world} GPU(s): {part}; NCCL gather of "
+                            f"O + LSE inside the timed step"
+                            + (f", overlapped with compute in {args.gather_chunks} head chunks"
+                               if args.partition == "kv" and args.gather_chunks > 1 else "")
+                            if world > 1 else "1 GPU"),
             "l2": "512 MiB buffer written between timed steps (L2 126 MB)",
             "seed": args.seed}
 
@@ -233,11 +236,59 @@ def owned_rows(args, M, world, rank):
     return None
 
 
+class ChunkedKvStep:
+    """A KV-group shard computed as `chunks` chunks of its Q heads (each its own PrefillRunner over
+    the shared K/V), each chunk's O / LSE sent to every peer while the next chunk computes
+    (shard.OverlappedHeadGather: NCCL point-to-point into the final layout)."""
+
+    def __init__(self, fp, shard, args, q, k, v, cfg, s, chunks):
+        ql, kl, vl = shard.local_slices(q, k, v, s)
+        self.ranges = shard.head_chunks(s.hq, chunks)
+        self.runners = [fp.PrefillRunner(ql[:, a:b].contiguous(), kl, vl, cfg,
+                                         out_dtype=torch.bfloat16) for a, b in self.ranges]
+        self.out = torch.empty(q.shape, dtype=torch.bfloat16, device=q.device)
+        self.lse = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
+        self.gather = shard.OverlappedHeadGather(args.hq, args.hkv, self.out, self.lse)
+
+    def capture(self):
+        for r in self.runners:
+            r.capture()
+        return self
+
+    @property
+    def graphs(self):
+        return [g for r in self.runners for g in r.graphs]
+
+    def check(self):
+        return sum(r.check() for r in self.runners)
+
+    def plans(self):
+        return [(r.counts, r.idx) for r in self.runners]
+
+    def step(self, stream=None, marks=None):
+        """One step; marks (list) collects (discover-end, attend-end) events per chunk."""
+        for (a, b), r in zip(self.ranges, self.runners):
+            r.replay_discover()
+            if marks is not None:
+                marks.append(torch.cuda.Event(enable_timing=True))
+                marks[-1].record(stream)
+            r.replay_attend()
+            if marks is not None:
+                marks.append(torch.cuda.Event(enable_timing=True))
+                marks[-1].record(stream)
+            self.gather.post(a, b, r.out, r.lse)
+        self.gather.wait()
+
+
 def make_runner(fp, args, q, k, v, cfg, world, rank):
     """This rank's PrefillRunner (its shard of the layer) and a gather closure."""
     from paper_2603_06199_b200 import shard
     if world == 1:
         return fp.PrefillRunner(q, k, v, cfg, out_dtype=torch.bfloat16), None, (0, args.hq)
+    if args.partition == "kv" and args.gather_chunks > 1 and q.shape[0] == 1:
+        s = shard.kv_group_shard(args.hq, args.hkv, world, rank)
+        return (ChunkedKvStep(fp, shard, args, q, k, v, cfg, s, args.gather_chunks), None,
+                (s.q_lo, s.q_hi))
     if args.partition == "kv":
         s = shard.kv_group_shard(args.hq, args.hkv, world, rank)
         ql, kl, vl = shard.local_slices(q, k, v, s)
@@ -253,10 +304,51 @@ def make_runner(fp, args, q, k, v, cfg, world, rank):
     return r, lambda: g(r.out, r.lse, B), (0, args.hq)
 
 
+def do_step(runner, gather=None):
+    if isinstance(runner, ChunkedKvStep):
+        runner.step()
+        return
+    runner.replay_discover()
+    runner.replay_attend()
+    if gather:
+        gather()
+
+
+def plan_totals(runner, rows):
+    """(algorithmic FLOPs, visits, diagonal visits) of this rank's plan(s)."""
+    plans = runner.plans() if isinstance(runner, ChunkedKvStep) else [(runner.counts, runner.idx)]
+    tot = [0.0, 0, 0]
+    for counts, idx in plans:
+        f, vis, diag = plan_flops(counts, idx, rows)
+        tot = [tot[0] + f, tot[1] + vis, tot[2] + diag]
+    return tot
+
+
 def time_runner(runner, stream, flush, reps, gather=None, dist=None):
     """CUDA-event times (ms lists) of discover, attend, gather and the whole step, L2 flushed
-    between steps."""
+    between steps.  For a ChunkedKvStep, discover / attend are summed over the chunks and
+    `gather` is the exposed part of the transfers (step minus compute)."""
     ts = {"step": [], "disc": [], "attn": [], "gather": []}
+    if isinstance(runner, ChunkedKvStep):
+        for _ in range(reps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if dist:
+                dist.barrier()
+            marks = []
+            e0.record(stream)
+            runner.step(stream, marks)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            starts = [e0] + marks[1::2][:-1]
+            disc = sum(a.elapsed_time(b) for a, b in zip(starts, marks[0::2]))
+            attn = sum(a.elapsed_time(b) for a, b in zip(marks[0::2], marks[1::2]))
+            step = e0.elapsed_time(e1)
+            ts["step"].append(step)
+            ts["disc"].append(disc)
+            ts["attn"].append(attn)
+            ts["gather"].append(step - disc - attn)
+        return ts
     for _ in range(reps):
         flush.fill_(1)  # evict L2 between steps (not timed)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -387,10 +479,7 @@ def run_gpu_arm(args, rank, world, dist):
     runner, gather, (q_lo, q_hi) = make_runner(fp, args, q, k, v, cfg, world, rank)
     runner.capture()
     for _ in range(args.warmup):
-        runner.replay_discover()
-        runner.replay_attend()
-        if gather:
-            gather()
+        do_step(runner, gather)
     torch.cuda.synchronize()
     runner.check()  # PlanError surfaces here (plans come from discovery: never expected)
 
@@ -406,7 +495,7 @@ def run_gpu_arm(args, rank, world, dist):
     per_rank = [mine]
     ms, ms_disc, ms_attn, ms_gather = mine
     rows = owned_rows(args, M, world, rank)
-    f_alg, visits, diag = plan_flops(runner.counts, runner.idx, rows)
+    f_alg, visits, diag = plan_totals(runner, rows)
     if dist:  # max over ranks; per-rank list; plan totals summed
         cd = _coll_device(dist, dev)
         allr = [torch.zeros(4, dtype=torch.float64, device=cd) for _ in range(world)]
@@ -574,6 +663,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fpb200", choices=["fpb200", "reference"])
     ap.add_argument("--partition", default="kv", choices=["kv", "rows", "zigzag"])
+    ap.add_argument("--gather-chunks", type=int, default=2,
+                    help="kv partition, N > 1: compute a rank's Q heads in this many chunks and "
+                         "send each chunk's O/LSE while the next computes (1 = one all-gather "
+                         "after all kernels)")
     ap.add_argument("--L", type=int, default=32768)
     ap.add_argument("--hq", type=int, default=32)
     ap.add_argument("--hkv", type=int, default=4)

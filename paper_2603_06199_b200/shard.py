@@ -108,6 +108,78 @@ def gather_heads(out_local: torch.Tensor, lse_local: torch.Tensor, Hq: int, Hkv:
     return out, lse
 
 
+def head_chunks(hl: int, chunks: int) -> list[tuple[int, int]]:
+    """A rank's hl local Q heads as `chunks` contiguous ranges (sizes differ by at most one)."""
+    chunks = max(1, min(chunks, hl))
+    per, extra = divmod(hl, chunks)
+    out, lo = [], 0
+    for c in range(chunks):
+        hi = lo + per + (1 if c < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+class OverlappedHeadGather:
+    """The O / LSE all-gather of a KV-group-sharded layer (Z = 1), posted chunk by chunk so it
+    runs on the collective stream while the rank computes its next chunk of Q heads.
+
+    Every rank owns the same number of Q heads (kv_group_shard), split the same way into chunks, so
+    chunk c of rank p lands at heads [q_lo(p) + a_c, q_lo(p) + b_c) of the full layer.  post(c, ...)
+    sends this rank's chunk to every peer and receives every peer's chunk straight into `out` /
+    `lse` with point-to-point operations (one NCCL group: no staging buffer, no permuting copy);
+    wait() makes the current stream wait for everything posted.  Over gloo (the CPU tests and the
+    shared-GPU test mode) the transfers are staged through host memory and complete in post()."""
+
+    def __init__(self, Hq: int, Hkv: int, out: torch.Tensor, lse: torch.Tensor, group=None):
+        import torch.distributed as dist
+        if out.shape[0] != 1:
+            raise ValueError("the overlapped gather needs Z = 1 (heads contiguous per rank)")
+        self.dist, self.group = dist, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.q_lo = [kv_group_shard(Hq, Hkv, self.world, r).q_lo for r in range(self.world)]
+        self.out, self.lse = out, lse
+        self.gloo = dist.get_backend(group) == "gloo"
+        self.works = []
+
+    def post(self, lo: int, hi: int, out_c: torch.Tensor, lse_c: torch.Tensor) -> None:
+        """This rank's local heads [lo, hi) (out_c: 1 x (hi-lo) x L x d, lse_c: 1 x (hi-lo) x L)."""
+        d = self.dist
+        me = self.q_lo[self.rank]
+        self.out[:, me + lo:me + hi].copy_(out_c)
+        self.lse[:, me + lo:me + hi].copy_(lse_c)
+        peers = [p for p in range(self.world) if p != self.rank]
+        if self.gloo:  # host-staged, synchronous
+            src_o, src_l = out_c.contiguous().cpu(), lse_c.contiguous().cpu()
+            for step in range(1, self.world):  # pairwise exchange, deadlock-free ring order
+                to, frm = (self.rank + step) % self.world, (self.rank - step) % self.world
+                ro = torch.empty_like(src_o)
+                rl = torch.empty_like(src_l)
+                ops = [d.P2POp(d.isend, src_o, to, self.group), d.P2POp(d.irecv, ro, frm, self.group),
+                       d.P2POp(d.isend, src_l, to, self.group), d.P2POp(d.irecv, rl, frm, self.group)]
+                for w in d.batch_isend_irecv(ops):
+                    w.wait()
+                q0 = self.q_lo[frm]
+                self.out[:, q0 + lo:q0 + hi].copy_(ro)
+                self.lse[:, q0 + lo:q0 + hi].copy_(rl)
+            return
+        ops = []
+        src_o, src_l = out_c.contiguous(), lse_c.contiguous()
+        for p in peers:
+            q0 = self.q_lo[p]
+            ops += [d.P2POp(d.isend, src_o, p, self.group),
+                    d.P2POp(d.irecv, self.out[:, q0 + lo:q0 + hi], p, self.group),
+                    d.P2POp(d.isend, src_l, p, self.group),
+                    d.P2POp(d.irecv, self.lse[:, q0 + lo:q0 + hi], p, self.group)]
+        self.works += d.batch_isend_irecv(ops)
+
+    def wait(self) -> None:
+        for w in self.works:
+            w.wait()
+        self.works = []
+
+
 # ----------------------------------------------------------------------------- row sharding
 # Strong scaling without the KV-group imbalance: rank r of G owns query blocks r, r + G, ...
 # of EVERY head (fpb_discover_select_rows / fpb_block_sparse_attention_rows with

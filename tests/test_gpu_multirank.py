@@ -47,6 +47,21 @@ def _worker(rank, world, port, part, shape, ret):
         r.replay_discover()
         r.replay_attend()
         out, lse = shard.gather_heads(r.out, r.lse, Hq, Hkv)
+    elif part == "kv_chunked":  # bench.py's overlapped gather: head chunks, P2P per chunk
+        s = shard.kv_group_shard(Hq, Hkv, world, rank)
+        ql, kl, vl = shard.local_slices(q, k, v, s)
+        out = torch.empty(q.shape, dtype=torch.bfloat16, device="cuda")
+        lse = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+        g = shard.OverlappedHeadGather(Hq, Hkv, out, lse)
+        rs = []
+        for a, b in shard.head_chunks(s.hq, 2):
+            r = fp.PrefillRunner(ql[:, a:b].contiguous(), kl, vl, cfg).capture()
+            r.replay_discover()
+            r.replay_attend()
+            g.post(a, b, r.out, r.lse)
+            rs.append(r)
+        g.wait()
+        r = rs[0]
     else:
         rows = shard.row_shard(world, rank) if part == "rows" else shard.zigzag_shard(world, rank)
         r = fp.PrefillRunner(q, k, v, cfg, rows=rows).capture()
@@ -65,6 +80,8 @@ def _worker(rank, world, port, part, shape, ret):
 @pytest.mark.parametrize("part,world,shape", [
     ("kv", 2, (8, 2, 2048)),     # one KV group per rank
     ("kv", 4, (8, 2, 2048)),     # world > Hkv: each group's 4 Q heads split 2 + 2
+    ("kv_chunked", 2, (8, 2, 2048)),  # 4 Q heads per rank in 2 chunks, P2P gather per chunk
+    ("kv_chunked", 4, (12, 2, 1000)),  # 3 Q heads per rank: chunks of 2 + 1, ragged L
     ("rows", 2, (8, 2, 3000)),   # interleaved query blocks, ragged last block
     ("zigzag", 3, (8, 2, 3000)),
 ])
@@ -82,15 +99,16 @@ def test_sharded_layer_gathers_bit_identical(fp, part, world, shape):
     assert torch.equal(ret["lse"], r.lse.cpu()), part
 
 
-@pytest.mark.parametrize("part", ["kv", "rows"])
-def test_bench_two_ranks_shared_gpu(fp, part):
+@pytest.mark.parametrize("part,chunks", [("kv", 2), ("kv", 1), ("rows", 1)])
+def test_bench_two_ranks_shared_gpu(fp, part, chunks):
     """bench.py --gpus 2 under torchrun (shared-GPU gloo mode): one strong-scaling JSON line with
-    per-rank times and the gather inside the step."""
+    per-rank times and the gather inside the step (kv: chunked P2P gather overlapped with the
+    next chunk's compute, or one all-gather after all kernels)."""
     env = dict(os.environ, FPB_BENCH_SHARED_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
            "--gpus", "2", "--steps", "3", "--warmup", "3", "--L", "8192", "--no-e2e",
-           "--partition", part]
+           "--partition", part, "--gather-chunks", str(chunks)]
     res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-3000:]
     lines = [x for x in res.stdout.splitlines() if x.startswith("{")]

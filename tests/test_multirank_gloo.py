@@ -140,3 +140,40 @@ def test_zigzag_blocks_partition(M, world):
     assert sorted(b for o in owned for b in o) == list(range(M))
     c = -(-M // (2 * world))
     assert all(len(o) <= 2 * c for o in owned)
+
+
+def _overlap_worker(rank, world, port, Hq, Hkv, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_06199_b200 import shard
+    L, d = 40, 8
+    full = torch.arange(Hq * L * d, dtype=torch.float32).view(1, Hq, L, d)
+    full_l = -torch.arange(Hq * L, dtype=torch.float32).view(1, Hq, L)
+    s = shard.kv_group_shard(Hq, Hkv, world, rank)
+    out, lse = torch.zeros_like(full), torch.zeros_like(full_l)
+    g = shard.OverlappedHeadGather(Hq, Hkv, out, lse)
+    for a, b in shard.head_chunks(s.hq, 2):  # bench.py's chunked KV step: P2P per head chunk
+        g.post(a, b, full[:, s.q_lo + a:s.q_lo + b], full_l[:, s.q_lo + a:s.q_lo + b])
+    g.wait()
+    ret[rank] = bool(torch.equal(out, full) and torch.equal(lse, full_l))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,Hq,Hkv", [(2, 8, 2), (4, 8, 2), (4, 12, 2), (3, 6, 3)])
+def test_overlapped_head_gather(world, Hq, Hkv):
+    """shard.OverlappedHeadGather (the chunked P2P gather bench.py overlaps with compute) puts
+    every rank's head chunks at their place in the full layer, on every rank."""
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_overlap_worker, args=(world, _free_port(), Hq, Hkv, ret), nprocs=world, join=True)
+    assert all(ret[r] for r in range(world)), dict(ret)
+
+
+def test_head_chunks():
+    from paper_2603_06199_b200.shard import head_chunks
+    assert head_chunks(4, 2) == [(0, 2), (2, 4)]
+    assert head_chunks(3, 2) == [(0, 2), (2, 3)]
+    assert head_chunks(1, 4) == [(0, 1)]
+    assert head_chunks(16, 3) == [(0, 6), (6, 11), (11, 16)]

@@ -2,7 +2,7 @@
 """FlashPrefill B200 benchmark — sparse-prefill attention on the Qwen3-30B-A3B layer shape.
 
 One step = the whole FlashPrefill hot path over ONE synthetic Qwen3 layer resident in HBM:
-  fpb_discover_select (K1 pooling + K2/K3 fused tcgen05 discovery, threshold, compaction)
+  fpb_discover_select (K1 pooling inside the K2/K3 tcgen05 discovery launch, threshold, compaction)
   -> fpb_block_sparse_attention (K4 tcgen05 block-sparse FlashAttention)
   -> (N > 1) the all-gather of O and LSE across ranks (NCCL), inside the timed region.
 Metric: effective TFLOP/s = dense-causal-equivalent FLOPs 4*d*Z*Hq*L(L+1)/2 of the layer / step
@@ -583,7 +583,7 @@ def run_gpu_arm(args, rank, world, dist):
         + M * M * args.hq * 4 + M * args.hq * 4
     traffic_cfg = {"L": args.L, "hq": args.hq, "hkv": args.hkv, "alpha": args.alpha,
                    "seed": args.seed}
-    launches = kernel_launches(runner, 4)
+    launches = kernel_launches(runner, 3)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -604,7 +604,7 @@ def run_gpu_arm(args, rank, world, dist):
                      "traffic_unit": "DRAM bytes per step of this kernel (ncu --set full, cold L2; summed over its launches: one per KV-range phase)",
                      "kernel": "fa_kernel (K4, csrc/attention_fa.cu)"
                                + (" on rank 0's shard" if world > 1 else "")},
-        "discovery_roofline": {"bound": "hbm", "kernel": "pool_keys + discover_kernel + select",
+        "discovery_roofline": {"bound": "hbm", "kernel": "discover_kernel (pools K in-kernel) + select_rows",
                                "traffic": ncu_traffic("discover_kernel", traffic_cfg),
                                "achieved": disc_bytes / (ms_disc * 1e-3) / 1e9,
                                "peak": pk["hbm"], "unit": "GB/s",

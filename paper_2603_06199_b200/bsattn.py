@@ -317,7 +317,8 @@ def normalize_block_scores(energies: BlockEnergies, grid: BlockGrid,
 
 def discover(queries: torch.Tensor, keys: torch.Tensor, grid: BlockGrid, tau: float,
              epsilon: float = kDefaultEpsilon, maps: bool = True) -> BlockScoreMap:
-    """discovery.hpp:153-159 (pool + fused approximation + normalisation in two launches).
+    """discovery.hpp:153-159 (pooling + approximation + normalisation: one discovery launch for
+    bf16 keys, which pools K in-kernel; fp32 keys are pooled by a separate launch).
 
     maps=False skips materialising energy/local_max (score only)."""
     _check_qk(queries, keys)

@@ -161,7 +161,8 @@ size_t ws_discover(const Dims& D, fpb_dtype t) {
     return align_up(pooled_bytes(D)) + 3 * align_up(map_elems(D) * 4) + align_up(map_elems(D));
   size_t b = kSchedBytes + align_up(kbar_split_bytes(D)) + align_up(discover_scratch_bytes(D));
   if (t == FPB_F32) b += align_up(2 * q_elems(D) * 2);
-  return b + (D.M < 1024 ? align_up(discover_rows_bytes(D)) : 0);  // two-pass plan-only mode
+  b += D.M < 1024 ? align_up(discover_rows_bytes(D)) : 0;  // two-pass plan-only mode
+  return b + align_up(discover_pool_ctr_bytes(D));         // in-kernel pooling counters
 }
 struct DiscWs {
   int* sched;
@@ -169,6 +170,7 @@ struct DiscWs {
   float* mscratch;         // long sequences only (discover_scratch_bytes)
   __nv_bfloat16* qplanes;  // fp32 inputs only
   float2* rows;            // two-pass plan-only mode (discover_rows_bytes)
+  int* pool_ctr;           // in-kernel pooling (bf16 keys): claim + per-chunk counters
 };
 DiscWs disc_ws(const Dims& D, void* ws, fpb_dtype t = FPB_BF16) {
   uint8_t* w = static_cast<uint8_t*>(ws);
@@ -176,9 +178,13 @@ DiscWs disc_ws(const Dims& D, void* ws, fpb_dtype t = FPB_BF16) {
   const size_t sb = discover_scratch_bytes(D);
   const size_t o2 = o1 + align_up(sb);
   const size_t o3 = o2 + (t == FPB_F32 ? align_up(2 * q_elems(D) * 2) : 0);
+  const size_t o4 = o3 + (D.M < 1024 ? align_up(discover_rows_bytes(D)) : 0);
   return {reinterpret_cast<int*>(w), reinterpret_cast<__nv_bfloat16*>(w + kSchedBytes),
           sb ? reinterpret_cast<float*>(w + o1) : nullptr,
-          reinterpret_cast<__nv_bfloat16*>(w + o2), reinterpret_cast<float2*>(w + o3)};
+          reinterpret_cast<__nv_bfloat16*>(w + o2), reinterpret_cast<float2*>(w + o3),
+          // the counters share the work counter's zeroed block when they fit (one memset)
+          discover_pool_ctr_bytes(D) + sizeof(int) <= kSchedBytes ? reinterpret_cast<int*>(w) + 1
+                                                                  : reinterpret_cast<int*>(w + o4)};
 }
 // attention: [sched][plan-row scratch] + fp32: Q hi/lo, K hi/lo, V bf16
 size_t ws_attention(const Dims& D, fpb_dtype t) {
@@ -201,10 +207,11 @@ int need_ws(size_t have, size_t need, void* ws) {
   return FPB_OK;
 }
 
-// Discovery front half: pool k̄ (+split) and stage Q planes; returns the Q plane pointer.
+// Discovery front half for fp32 inputs: pool k̄ (+split) and stage the Q planes; returns the Q
+// plane pointer.  bf16 inputs need nothing: the discovery kernel pools K itself.
 int discover_prepare(const Dims& D, fpb_dtype t, const void* Q, const void* K, float* pooled,
                      const DiscWs& w, cudaStream_t st, const __nv_bfloat16** q_planes) {
-  FPB_CUDA(launch_pool_keys(D, t == FPB_BF16, K, pooled, w.kbar, st));
+  if (t == FPB_F32) FPB_CUDA(launch_pool_keys(D, false, K, pooled, w.kbar, st));
   if (t == FPB_BF16) {
     *q_planes = static_cast<const __nv_bfloat16*>(Q);
   } else {
@@ -382,8 +389,10 @@ static int discover_select_rows(const fpb_problem* p, int32_t row_begin, int32_t
   // per-item tail (32K: 0.133 -> 0.126 ms; no gain for longer rows, profiles/r1_ab_disc_two_pass)
   if (FPB_DISC_TWO_PASS && D.M < 1024 && idx && !energy && !local_max && !score && !mask)
     o.rows = w.rows;
+  const bool fused_pool = dtype == FPB_BF16;  // the discovery kernel pools the bf16 keys itself
   FPB_CUDA(launch_discover(D, dtype == FPB_F32 ? 2 : 1, qp, w.kbar, o, w.sched, w.mscratch,
-                           S(stream)));
+                           S(stream), fused_pool ? static_cast<const __nv_bfloat16*>(K) : nullptr,
+                           nullptr, w.pool_ctr));
   return FPB_OK;
 }
 

@@ -15,6 +15,15 @@
 // accumulating MMAs); bf16 Q is exact.  fp32 Q (the C1 config) is split too (3 MMAs: hh, hl, lh).
 // Naively rounding k̄ to bf16 flips mask bits (SURVEY §7 hard part 1).
 //
+// Pooling (discovery.hpp:39-70) runs in the same launch for bf16 keys: every CTA first claims
+// (z, kv head, key block) units from a global counter, stages each block's 128 contiguous K rows
+// in shared memory with one bulk copy (TMA engine; two in flight per warpgroup), sums one channel
+// per thread in the reference's order and writes the k̄ hi/lo planes, then publishes the block
+// on a per-(kv head, 128-block chunk) counter (release).  The TMA producer acquires a chunk's
+// counter before its first k̄ load of that chunk.  Units are claimed dynamically and a CTA waits
+// only after the claims ran out, so every claimed unit belongs to a running CTA: no co-residency
+// assumption, no deadlock with concurrent kernels.
+//
 // Warp roles (384 threads, persistent):
 //   w2  TMEM allocator (512 cols), then scheduler + TMA producer: item ring (with each item's
 //       chunk count), Q tiles (double-buffered), k̄ chunk ring
@@ -23,6 +32,7 @@
 //   w4..w7, w8..w11  two epilogue warpgroups, items alternating: TMEM -> (m, S) per pair, then
 //          row normalisation, threshold and compaction for the item while the MMA warp and the
 //          other warpgroup already work on the next ones.
+#include <cstddef>
 #include <cstdlib>
 
 #include "fp_kernels.h"
@@ -38,6 +48,7 @@ constexpr int kEpiThreads = 128;               // per epilogue warpgroup (two of
 constexpr int kTile = kBlock * kHeadDim * 2;  // one bf16 128x128 operand tile: 32 KiB
 constexpr int kStages = 2;                    // k̄ chunk ring (hi + lo per stage)
 constexpr int kItemRing = 4;
+constexpr int kPoolTiles = 6;  // in-kernel pooling staging ring (the q and kb tiles of NQ = 1)
 constexpr uint32_t kEpiBar = 1;               // named barriers 1, 2: the two epilogue warpgroups
 // Control roles sit on the SM sub-partitions whose epilogue warps are least loaded: epilogue warp
 // w4 + i serves key blocks J = 32i..32i+31 of a chunk, and short causal chunks leave the high
@@ -62,6 +73,12 @@ struct DiscParams {
   int num_items;
   int prefilled;   // idx rows already hold the fill value N (launch_fill_plan)
   float* mscratch;  // per-CTA m/S rows in global memory when they do not fit in shared memory
+  // in-kernel pooling (bf16 keys): K, the k̄ hi/lo destination, optional fp32 k̄, and the zeroed
+  // counters [claim, pooled blocks per (z * Hkv + kv, chunk)]; kpool == nullptr: k̄ is given
+  const __nv_bfloat16* kpool;
+  __nv_bfloat16* kbar;
+  float* pooled;
+  int* pool_ctr;
 };
 
 template <int NQ>
@@ -78,9 +95,16 @@ struct DiscSmem {
   int lastlive[kItemRing];  // causal key blocks of its last chunk (I % 128 + 1)
   uint32_t tmem_base;
   float red[2][3][4];
+  uint64_t pool_full[6], pool_empty[6];  // in-kernel pooling: 6 staging tiles over q and kb
+  int pool_unit[6];
   // followed by float m_s[M], S_s[M] per epilogue warpgroup, then int counts[ceil(M/128)][4]
   // per epilogue warpgroup (dynamic)
 };
+
+// the in-kernel pooling ring spans the q and kb tiles of the bf16 (NQ = 1) layout
+static_assert(offsetof(DiscSmem<1>, kb) == offsetof(DiscSmem<1>, q) + 2 * kTile &&
+                  sizeof(DiscSmem<1>::q) + sizeof(DiscSmem<1>::kb) == kPoolTiles * kTile,
+              "pooling tiles");
 
 __device__ __forceinline__ void decode_item(const Dims& D, int item, int& z, int& h, int& I) {
   h = item % D.Hq;  // h fastest: co-running CTAs fill the head-last plan rows of one (z, I)
@@ -91,8 +115,8 @@ __device__ __forceinline__ void decode_item(const Dims& D, int item, int& z, int
 
 #ifdef FPB_TRACE
 // cycle accounting (tools/trace_discover.py): per-thread accumulators, lane 0 of each warp flushes
-__device__ unsigned long long g_dtrace[24];
-#define DT_DECL unsigned long long dt_acc[24] = {}; long long _dt = 0
+__device__ unsigned long long g_dtrace[32];
+#define DT_DECL unsigned long long dt_acc[32] = {}; long long _dt = 0
 #define DT_T0() _dt = clock64()
 #define DT_ADD(i)                                \
   do {                                           \
@@ -103,7 +127,7 @@ __device__ unsigned long long g_dtrace[24];
 #define DT_FLUSH()                                                         \
   do {                                                                     \
     if (lane_id() == 0)                                                    \
-      for (int _i = 0; _i < 24; ++_i)                                      \
+      for (int _i = 0; _i < 32; ++_i)                                      \
         if (dt_acc[_i]) atomicAdd(&g_dtrace[_i], dt_acc[_i]);              \
   } while (0)
 #else
@@ -128,6 +152,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   DT_DECL;
 #ifdef FPB_TRACE
   const long long t_begin = clock64();
+  auto gtimer = [] {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+  };
+  if (threadIdx.x == 0) {  // CTA start spread (globaltimer ns): [28] = ~min, [29] = max
+    const unsigned long long t0 = gtimer();
+    atomicMax(&g_dtrace[28], ~t0);
+    atomicMax(&g_dtrace[29], t0);
+  }
 #endif
 
   if (threadIdx.x == 0) {
@@ -149,6 +183,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&s.it_full[i]), 1);
       mbar_init(smem_u32(&s.it_empty[i]), 1 + 4);  // MMA thread + the owning epilogue warpgroup
     }
+    for (int t = 0; t < kPoolTiles; ++t) {
+      mbar_init(smem_u32(&s.pool_full[t]), 1);
+      mbar_init(smem_u32(&s.pool_empty[t]), 1);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(smem_u32(&s.tmem_base));
@@ -156,11 +194,137 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s.tmem_base;
+  const int nck = (D.M + kBlock - 1) / kBlock;
+
+  if constexpr (NQ == 1) {
+    if (prm.kpool) {
+      // ===================== pooling (discovery.hpp:39-70).  Warp 0 lane 0 claims units (one
+      // k̄ block each) in batches from the global counter and streams them with bulk copies into
+      // a 6-tile ring over the (still unused) q and kb tiles; the two epilogue warpgroups take
+      // alternate tiles, one channel per thread, and publish each block on its chunk counter.
+      const int units = D.Z * D.Hkv * D.M;
+      const uint32_t stage0 = smem_u32(s.q);
+      if (warp == 0) {
+        if (lane == 0) {
+          // guided self-scheduling: each claim takes half the fair share of what is left, so the
+          // CTAs that start first cannot take whole shares that later CTAs then wait for
+          int next_u = 0, have = 0, ends = 0;
+          for (int k = 0; ends < 2; ++k) {
+            const int t = k % kPoolTiles;
+            DT_T0();
+            if (k >= kPoolTiles) mbar_wait(smem_u32(&s.pool_empty[t]), ((k / kPoolTiles) - 1) & 1);
+            DT_ADD(25);  // pooling loader: waiting for a free tile
+            int u = units;
+            if (!ends) {
+              if (have == 0) {
+                const int batch = min(16, max(1, (units - next_u) / (2 * (int)gridDim.x)));
+                next_u = atomicAdd(prm.pool_ctr, batch);
+                have = batch;
+              }
+              u = next_u++;
+              --have;
+            }
+            DT_ADD(24);  // pooling loader: claims
+            const uint32_t fb = smem_u32(&s.pool_full[t]);
+            if (u >= units) {  // one end marker per consumer warpgroup (k, k + 1)
+              s.pool_unit[t] = -1;
+              mbar_arrive(fb);
+              ++ends;
+              continue;
+            }
+            s.pool_unit[t] = u;
+            const int zkv = u / D.M, j = u % D.M;
+            const uint32_t bytes = (uint32_t)(block_len(D, j) * kHeadDim * 2);
+            mbar_arrive_expect_tx(fb, bytes);
+            bulk_load_1d(stage0 + t * kTile,
+                         prm.kpool + ((size_t)zkv * D.L + (size_t)j * kBlock) * kHeadDim, bytes, fb);
+          }
+        }
+      } else if (warp >= 4) {
+        const int g = (warp - 4) >> 2, c = threadIdx.x & 127;
+        const size_t plane = (size_t)D.Z * D.Hkv * D.M * kHeadDim;
+        // blocks are published per chunk run: one proxy fence + release per run of consecutive
+        // units of the same (kv head, chunk), not per block
+        int run_key = -1, run_len = 0;
+        auto publish = [&]() {
+          if (run_len == 0) return;
+          fence_proxy_async_global();  // k̄ is read by TMA (async proxy), in other CTAs
+          named_bar_sync(3 + g, 128);
+          if (c == 0) {
+            __threadfence();
+            red_add_release_gpu(prm.pool_ctr + 1 + run_key, run_len);
+          }
+          run_len = 0;
+        };
+        for (int k = g;; k += 2) {
+          const int t = k % kPoolTiles;
+          DT_T0();
+          mbar_wait(smem_u32(&s.pool_full[t]), (k / kPoolTiles) & 1);
+          DT_ADD(25);  // pooling: waiting for the block's rows
+          const int u = s.pool_unit[t];
+          if (u < 0) break;
+          const int zkv = u / D.M, j = u % D.M, len = block_len(D, j);
+          const int key = zkv * nck + j / kBlock;
+          if (key != run_key) {
+            publish();
+            run_key = key;
+          }
+          // channel c of row r at stage + 2 (r d + c); explicit ld.shared (the aligned Smem view
+          // hides the address space from the compiler)
+          const uint32_t col = stage0 + t * kTile + 2 * c;
+          auto row = [&](int r) {
+            uint16_t x;
+            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(x) : "r"(col + r * 2 * kHeadDim));
+            return __bfloat162float(__ushort_as_bfloat16(x));
+          };
+          float sum = 0.f;  // discovery.hpp:51-53: out[c] += row[c], r ascending
+          if (len == kBlock) {
+#pragma unroll 32
+            for (int r = 0; r < kBlock; ++r) sum = __fadd_rn(sum, row(r));
+          } else {
+            for (int r = 0; r < len; ++r) sum = __fadd_rn(sum, row(r));
+          }
+          DT_ADD(26);  // pooling: channel sums
+          const float o = __fmul_rn(sum, __fdiv_rn(1.0f, (float)len));  // discovery.hpp:55-56
+          const size_t dst = ((size_t)zkv * D.M + j) * kHeadDim + c;
+          if (prm.pooled) prm.pooled[dst] = o;
+          const __nv_bfloat16 hi = __float2bfloat16_rn(o);
+          prm.kbar[dst] = hi;
+          prm.kbar[plane + dst] = __float2bfloat16_rn(__fsub_rn(o, __bfloat162float(hi)));
+          fence_proxy_async_smem();  // the tile is refilled by a bulk copy
+          named_bar_sync(3 + g, 128);
+          if (c == 0) mbar_arrive(smem_u32(&s.pool_empty[t]));
+          ++run_len;
+          DT_ADD(27);  // pooling: k̄ stores, tile release
+        }
+        publish();
+      }
+      __syncthreads();  // the staging tiles become the Q / k̄ rings
+#ifdef FPB_TRACE
+      if (threadIdx.x == 0) {
+        dt_acc[6] += (unsigned long long)(clock64() - t_begin);
+        atomicMax(&g_dtrace[30], gtimer());  // latest prologue end
+      }
+#endif
+    }
+  }
 
   if (warp == kProducerWarp) {
     // ===================== scheduler + TMA producer
     if (elect_one()) {
       int gc = 0;  // global chunk counter (same sequence as the MMA issuer)
+      uint64_t ready = 0;  // in-kernel pooling: k̄ chunks already seen complete (first 64 keys)
+      auto wait_pooled = [&](int zkv, int c) {
+        const int key = zkv * nck + c;
+        if (key < 64 && ((ready >> key) & 1)) return;
+        const int need = min(kBlock, D.M - c * kBlock);
+        while (ld_acquire_gpu(prm.pool_ctr + 1 + key) < need) __nanosleep(64);
+        fence_proxy_async_global();  // the acquired k̄ stores before this CTA's TMA reads
+        if (key < 64) ready |= 1ull << key;
+#ifdef FPB_TRACE
+        atomicMax(&g_dtrace[31], gtimer());  // latest first sight of a pooled chunk
+#endif
+      };
       for (int t = 0;; ++t) {
         const int slot = t % kItemRing;
         DT_T0();
@@ -201,6 +365,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           DT_T0();
           if (gc >= kStages) mbar_wait(smem_u32(&s.kb_empty[st]), ((gc / kStages) - 1) & 1);
           DT_ADD(14);  // producer: k̄ ring full
+          if (NQ == 1 && prm.kpool) wait_pooled(zkv, c);
+          DT_ADD(23);  // producer: waiting for in-kernel pooling
           const uint32_t fb = smem_u32(&s.kb_full[st]);
           mbar_arrive_expect_tx(fb, 2 * kTile);
           for (int sp = 0; sp < 2; ++sp)
@@ -510,7 +676,8 @@ cudaError_t launch_nq(const Dims& D, const CUtensorMap& tm_q, const CUtensorMap&
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int sms = sm_count();
-  const int grid = prm.num_items < sms ? prm.num_items : sms;
+  // in-kernel pooling wants every SM streaming K, whether or not it gets discovery items
+  const int grid = (prm.num_items < sms && !prm.kpool) ? prm.num_items : sms;
   discover_kernel<NQ><<<grid, kThreads, smem, s>>>(tm_q, tm_kb, prm);
   return cudaGetLastError();
 }
@@ -526,16 +693,28 @@ size_t discover_scratch_bytes(const Dims& D) {
   return (size_t)sm_count() * 2 * 2 * sizeof(float) * D.M;
 }
 
+size_t discover_pool_ctr_bytes(const Dims& D) {
+  return sizeof(int) * (1 + (size_t)D.Z * D.Hkv * ((D.M + kBlock - 1) / kBlock));
+}
+
 cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_planes,
-                            const __nv_bfloat16* kbar_split, const DiscoverOut& out, int* sched,
-                            float* mscratch, cudaStream_t s) {
+                            __nv_bfloat16* kbar_split, const DiscoverOut& out, int* sched,
+                            float* mscratch, cudaStream_t s, const __nv_bfloat16* kpool,
+                            float* pooled, int* pool_ctr) {
+  if (kpool && (q_splits != 1 || !pool_ctr)) return cudaErrorInvalidValue;
   if (discover_scratch_bytes(D) == 0) mscratch = nullptr;
   else if (!mscratch) return cudaErrorInvalidValue;
   CUtensorMap tm_q, tm_kb;
   if (!make_tmap_rows128(&tm_q, q_planes, D.L, (uint64_t)q_splits * D.Z * D.Hq) ||
       !make_tmap_rows128(&tm_kb, kbar_split, D.M, 2ull * D.Z * D.Hkv))
     return cudaErrorInvalidValue;
-  cudaError_t e = cudaMemsetAsync(sched, 0, sizeof(int), s);
+  cudaError_t e;
+  if (kpool && pool_ctr == sched + 1) {  // counters right behind the work counter: one memset
+    e = cudaMemsetAsync(sched, 0, sizeof(int) + discover_pool_ctr_bytes(D), s);
+  } else {
+    e = cudaMemsetAsync(sched, 0, sizeof(int), s);
+    if (e == cudaSuccess && kpool) e = cudaMemsetAsync(pool_ctr, 0, discover_pool_ctr_bytes(D), s);
+  }
   if (e != cudaSuccess) return e;
   // Long rows: the fill value N of the unused plan slots goes in first as coalesced 16-byte
   // stores (at 256K, one 4-byte store per slot at stride Hq from the epilogue costs as much as
@@ -546,7 +725,8 @@ cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_
     cudaError_t e = launch_fill_plan(D, out.idx, s);
     if (e != cudaSuccess) return e;
   }
-  DiscParams prm{D, out, sched, D.Z * D.Hq * D.Mr, prefilled, mscratch};
+  DiscParams prm{D,      out,        sched,  D.Z * D.Hq * D.Mr, prefilled, mscratch,
+                 kpool,  kbar_split, pooled, pool_ctr};
   e = q_splits == 1 ? launch_nq<1>(D, tm_q, tm_kb, prm, s) : launch_nq<2>(D, tm_q, tm_kb, prm, s);
   if (e != cudaSuccess || !out.rows) return e;
   return launch_select_rows(D, out.rows, out.idx, out.counts, prefilled != 0, s);
@@ -556,9 +736,9 @@ cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_
 
 #ifdef FPB_TRACE
 extern "C" int fpb_dtrace_read(unsigned long long* host24, int reset) {
-  cudaError_t e = cudaMemcpyFromSymbol(host24, fpb::g_dtrace, sizeof(unsigned long long) * 24);
+  cudaError_t e = cudaMemcpyFromSymbol(host24, fpb::g_dtrace, sizeof(unsigned long long) * 32);
   if (reset) {
-    unsigned long long z[24] = {};
+    unsigned long long z[32] = {};
     cudaMemcpyToSymbol(fpb::g_dtrace, z, sizeof(z));
   }
   return (int)e;

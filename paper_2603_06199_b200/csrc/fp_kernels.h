@@ -50,9 +50,14 @@ inline size_t discover_rows_bytes(const Dims& D) {
 }
 cudaError_t launch_select_rows(const Dims& D, const float2* rows, int32_t* idx, int32_t* counts,
                                bool prefilled, cudaStream_t s);
+// kpool != nullptr (bf16 keys, q_splits == 1): the kernel pools K itself into kbar_split (and
+// `pooled` if given), using the pool_ctr counters (discover_pool_ctr_bytes, zeroed here);
+// otherwise kbar_split already holds k̄.
 cudaError_t launch_discover(const Dims& D, int q_splits, const __nv_bfloat16* q_planes,
-                            const __nv_bfloat16* kbar_split, const DiscoverOut& out, int* sched,
-                            float* mscratch, cudaStream_t s);
+                            __nv_bfloat16* kbar_split, const DiscoverOut& out, int* sched,
+                            float* mscratch, cudaStream_t s, const __nv_bfloat16* kpool = nullptr,
+                            float* pooled = nullptr, int* pool_ctr = nullptr);
+size_t discover_pool_ctr_bytes(const Dims& D);
 // Global scratch launch_discover needs (0 while the per-key-block rows fit in shared memory,
 // i.e. up to ~270K tokens at B = 128).
 size_t discover_scratch_bytes(const Dims& D);

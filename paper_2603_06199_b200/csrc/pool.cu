@@ -18,14 +18,6 @@ namespace fpb {
 
 using namespace ptx;
 
-__device__ __forceinline__ void bulk_load_1d(uint32_t dst, const void* src, uint32_t bytes,
-                                             uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(dst), "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
-      : "memory");
-}
-
 template <bool kBf16>
 __global__ void __launch_bounds__(kHeadDim) pool_keys_kernel(const void* __restrict__ K,
                                                              float* __restrict__ pooled,

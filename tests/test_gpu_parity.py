@@ -71,6 +71,50 @@ def test_discover_maps(fp, port, case):
     assert rs[big].max() <= 5e-5, rs[big].max()
 
 
+@pytest.mark.parametrize("shape", [(1, 2, 2, 2048), (2, 6, 3, 1000), (1, 4, 1, 300)])
+def test_in_kernel_pooling_bit_identical(fp, port, shape):
+    """bf16 discovery pools K inside the discovery kernel (claimed blocks, per-chunk release /
+    acquire counters); the result must equal the two-launch path — pool_keys (bit-exact against
+    the oracle) then approx_block_scores on that k̄ — bit for bit, ragged last block and GQA
+    included."""
+    Z, Hq, Hkv, L = shape
+    q, k, _ = (bf16_round(x) for x in composite_np(7 + L, Z, Hq, Hkv, L))
+    grid = fp.make_block_grid(L, 128)
+    tau = float(port.scale(128))
+    pk = fp.pool_keys(_cuda(k), grid)
+    assert np.array_equal(_np(pk.data), port.pool_keys(k, 128))
+    two = fp.approx_block_scores(_cuda(q), pk, grid, tau)
+    one = fp.discover(_cuda(q), _cuda(k), grid, tau)
+    assert np.array_equal(_np(one.energy), _np(two.energy))
+    assert np.array_equal(_np(one.local_max), _np(two.local_max))
+
+
+def test_discovery_on_concurrent_streams(fp):
+    """Two streams run persistent discovery launches (one CTA per SM each, in-kernel pooling with
+    cross-CTA counters) at the same time, so each launch gets only part of the SMs; claims are
+    dynamic, so neither may wait on a pooling unit held by a CTA that is not running.  Plans equal
+    the single-stream ones."""
+    L = 8192
+    q, k, _ = (bf16_round(x) for x in composite_np(11, 1, 32, 4, L))
+    q2 = np.ascontiguousarray(q[:, ::-1])
+    cfg = fp.PipelineConfig()
+    ins = [(_cuda(q), _cuda(k)), (_cuda(q2), _cuda(k))]
+    ref = [fp.discover_select(a, b, cfg)[0] for a, b in ins]
+    ref = [(_np(p.indices), _np(p.counts)) for p in ref]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+    outs = [[], []]
+    for _ in range(6):
+        for i, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                outs[i].append(fp.discover_select(*ins[i], cfg)[0])
+    torch.cuda.synchronize()
+    for i in range(2):
+        for p in outs[i]:
+            assert np.array_equal(_np(p.indices), ref[i][0])
+            assert np.array_equal(_np(p.counts), ref[i][1])
+
+
 @pytest.mark.parametrize("alpha", [0.0, 0.05, 0.12, 0.5, 1.0])
 def test_threshold_and_compress_bitexact(fp, port, alpha):
     q, k, _ = _planted(port, 1, 300, 0, 4096, H=3)

@@ -9,10 +9,11 @@ Metric: effective TFLOP/s = dense-causal-equivalent FLOPs 4*d*Z*Hq*L(L+1)/2 of t
 time, max over ranks; ms_per_step is reported beside it.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl fpb200|reference] [--L 32768]
-                  [--partition kv|rows|zigzag]
+                  [--partition kv|kv_zigzag|rows|zigzag]
   N > 1 (torchrun, one rank per GPU): strong scaling of the one layer.  `kv` (default, north_star)
   gives rank g a KV-head group (kv_group_shard; with N > Hkv a group's Q heads are split and its
-  KV head replicated); `rows` / `zigzag` give every rank a share of every head's query blocks.
+  KV head replicated); `kv_zigzag` keeps one KV head per rank but splits a group's rows (zigzag)
+  instead of its Q heads; `rows` / `zigzag` give every rank a share of every head's query blocks.
   No collective inside the kernels; one all-gather of O + LSE after them.
 
 L2 hygiene: a 512 MiB buffer is written between timed steps (L2 is 126 MB); each step is timed
@@ -153,7 +154,9 @@ def bench_config(args, world):
     """The `config` object — identical in both arms (the driver compares them)."""
     part = {"kv": "KV-head-group shards (kv_group_shard)",
             "rows": "interleaved query-block shards (fpb_*_rows)",
-            "zigzag": "zigzag query-block shards (fpb_*_zigzag)"}[args.partition]
+            "zigzag": "zigzag query-block shards (fpb_*_zigzag)",
+            "kv_zigzag": "KV-head-group shards, a group's ranks split by zigzag query-block "
+                         "chunks (kv_zigzag_shard)"}[args.partition]
     return {"workload": f"Qwen3-30B-A3B attention layer (Hq={args.hq}, Hkv={args.hkv}, d=128) "
                         f"bf16 causal L={args.L}, alpha={args.alpha}, B=128, sink 256, window 512",
             "global_batch_sequences": 1, "seq_len": args.L,
@@ -233,6 +236,10 @@ def owned_rows(args, M, world, rank):
         return list(range(rank, M, world))
     if args.partition == "zigzag" and world > 1:
         return shard.zigzag_blocks(M, world, rank)
+    if args.partition == "kv_zigzag" and world > 1:
+        _, rows = shard.kv_zigzag_shard(args.hq, args.hkv, world, rank,
+                                        getattr(args, "kv_weights_used", None))
+        return None if rows is None else shard.zigzag_blocks(M, rows[2], rows[1])
     return None
 
 
@@ -280,6 +287,21 @@ class ChunkedKvStep:
         self.gather.wait()
 
 
+def kv_weights(fp, args, q, k, cfg, world):
+    """Per-KV-group work weights for --partition kv_zigzag --kv-weights plan: block visits of each
+    group's Q heads from one calibration discovery of the layer (outside the timed region; the
+    same on every rank: same inputs, deterministic plan).  None = equal ranks per group."""
+    if args.kv_weights != "plan" or world <= args.hkv:
+        return None  # at most one rank per group: nothing to weigh
+    plan = fp.discover_select(q, k, cfg)[0]
+    per_head = plan.counts.sum(dim=(0, 1)).double()  # Z x M x Hq -> per Q head
+    g = args.hq // args.hkv
+    w = [float(per_head[i * g:(i + 1) * g].sum()) for i in range(args.hkv)]
+    args.kv_weights_used = w
+    del plan
+    return w
+
+
 def make_runner(fp, args, q, k, v, cfg, world, rank):
     """This rank's PrefillRunner (its shard of the layer) and a gather closure."""
     from paper_2603_06199_b200 import shard
@@ -289,6 +311,16 @@ def make_runner(fp, args, q, k, v, cfg, world, rank):
         s = shard.kv_group_shard(args.hq, args.hkv, world, rank)
         return (ChunkedKvStep(fp, shard, args, q, k, v, cfg, s, args.gather_chunks), None,
                 (s.q_lo, s.q_hi))
+    if args.partition == "kv_zigzag":
+        w = kv_weights(fp, args, q, k, cfg, world)
+        s, rows = shard.kv_zigzag_shard(args.hq, args.hkv, world, rank, w)
+        ql, kl, vl = shard.local_slices(q, k, v, s)
+        r = fp.PrefillRunner(ql, kl, vl, cfg, out_dtype=torch.bfloat16, rows=rows)
+        out_full = torch.empty(q.shape, dtype=torch.bfloat16, device=q.device)
+        lse_full = torch.empty(q.shape[:3], dtype=torch.float32, device=q.device)
+        return r, lambda: shard.gather_kv_zigzag(r.out, r.lse, args.hq, args.hkv, B,
+                                                 out=out_full, lse=lse_full,
+                                                 weights=w), (s.q_lo, s.q_hi)
     if args.partition == "kv":
         s = shard.kv_group_shard(args.hq, args.hkv, world, rank)
         ql, kl, vl = shard.local_slices(q, k, v, s)
@@ -621,6 +653,10 @@ def run_gpu_arm(args, rank, world, dist):
         out["per_rank_ms"] = [{"step": r[0], "discover_select": r[1], "sparse_attention": r[2],
                                "gather": r[3]} for r in per_rank]
         out["partition"] = args.partition
+        if args.partition == "kv_zigzag" and getattr(args, "kv_weights_used", None):
+            from paper_2603_06199_b200 import shard
+            out["kv_group_ranks"] = shard.kv_group_ranks(args.hkv, world, args.kv_weights_used)
+            out["kv_group_visits"] = args.kv_weights_used
     if e2e_ms is not None:
         out["e2e"] = {"value": job_flops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT, "ms": e2e_ms,
                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -662,7 +698,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fpb200", choices=["fpb200", "reference"])
-    ap.add_argument("--partition", default="kv", choices=["kv", "rows", "zigzag"])
+    ap.add_argument("--partition", default="kv", choices=["kv", "kv_zigzag", "rows", "zigzag"])
+    ap.add_argument("--kv-weights", default="plan", choices=["plan", "equal"],
+                    help="kv_zigzag: ranks per KV group by the calibration plan's visits per "
+                         "group (plan) or world / Hkv each (equal)")
     ap.add_argument("--gather-chunks", type=int, default=2,
                     help="kv partition, N > 1: compute a rank's Q heads in this many chunks and "
                          "send each chunk's O/LSE while the next computes (1 = one all-gather "

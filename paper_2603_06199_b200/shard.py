@@ -7,6 +7,10 @@ data-path collective:
 * ``kv_group_shard`` — strong scaling of one batch by KV-head groups: rank g owns KV heads
   [g*Hkv/G, (g+1)*Hkv/G) and their Q heads; with G > Hkv each group's Q heads are split over
   G/Hkv ranks and the KV head is replicated (e.g. Qwen3 Hkv=4 on 8 GPUs: 4 Q heads per rank).
+* ``kv_zigzag_shard`` — the same KV-head groups, but with more ranks than KV heads a group is
+  split by zigzag query-block chunks (all of its Q heads on every rank of the group) instead of by
+  Q heads, so the ranks of a group carry equal work whatever the per-head densities
+  (``gather_kv_zigzag`` reassembles it).
 * ``unit_shard`` — weak scaling: work units (sequence, KV-head group) dealt contiguously.
 * ``gather_heads`` — the only collective: one all-gather of O and LSE along the head axis after
   all kernels complete (NCCL over NVLink in production, gloo in the CPU tests).
@@ -50,6 +54,51 @@ def kv_group_shard(Hq: int, Hkv: int, world: int, rank: int) -> HeadShard:
     per_q = g // split
     q0 = kv * g + (rank % split) * per_q
     return HeadShard(q0, q0 + per_q, kv, kv + 1)
+
+
+def kv_group_ranks(Hkv: int, world: int, weights=None) -> list[int]:
+    """Ranks per KV group for world >= Hkv: equal (world / Hkv each) without weights; with
+    per-group work weights (e.g. the plan's block visits per KV group from a calibration pass),
+    every group gets one rank and each further rank goes to the group with the largest work per
+    rank, so heavy groups are split over more ranks (profiles/r2_kv_zigzag.md)."""
+    if world < Hkv:
+        raise ValueError("fewer ranks than KV groups: use kv_group_shard")
+    if weights is None:
+        if world % Hkv:
+            raise ValueError(f"{world} ranks cannot split {Hkv} KV groups evenly")
+        return [world // Hkv] * Hkv
+    if len(weights) != Hkv:
+        raise ValueError("one weight per KV group")
+    n = [1] * Hkv
+    for _ in range(world - Hkv):
+        g = max(range(Hkv), key=lambda i: (weights[i] / n[i], -i))
+        n[g] += 1
+    return n
+
+
+def kv_zigzag_shard(Hq: int, Hkv: int, world: int, rank: int, weights=None):
+    """KV-head-group shard that splits a group by query rows instead of Q heads.
+
+    Returns (HeadShard, rows): with world <= Hkv (and no weights) it is kv_group_shard and rows is
+    None; otherwise the ranks of a KV group (kv_group_ranks: equal, or by work weights) each take
+    ALL of the group's Q heads but only the zigzag query-block chunks (sub, 2 n - 1 - sub) of an
+    n-rank zigzag partition (rows = ("zigzag", sub, n), fpb_*_zigzag).  A rank still holds exactly
+    one KV head (the north_star partition), but its work no longer depends on which Q heads it
+    drew: per-head densities differ several-fold (profiles/r2_lsweep.md)."""
+    if Hq % Hkv:
+        raise ValueError("Hq must be a multiple of Hkv")
+    if world <= Hkv and (weights is None or world < Hkv):
+        return kv_group_shard(Hq, Hkv, world, rank), None
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    n = kv_group_ranks(Hkv, world, weights)
+    g = Hq // Hkv
+    kv, first = 0, 0
+    while rank >= first + n[kv]:
+        first += n[kv]
+        kv += 1
+    rows = ("zigzag", rank - first, n[kv]) if n[kv] > 1 else None
+    return HeadShard(kv * g, (kv + 1) * g, kv, kv + 1), rows
 
 
 def unit_shard(n_units: int, world: int, rank: int) -> range:
@@ -270,3 +319,61 @@ def gather_rows(out: torch.Tensor, lse: torch.Tensor, block: int, group=None):
         full = full.view((x.shape[0], x.shape[1], -1) + tuple(x.shape[3:]))[:, :, :L]
         res.append(full.contiguous())
     return res[0], res[1]
+
+
+def gather_kv_zigzag(out_local: torch.Tensor, lse_local: torch.Tensor, Hq: int, Hkv: int,
+                     block: int, group=None, out: torch.Tensor | None = None,
+                     lse: torch.Tensor | None = None, weights=None):
+    """Gather a kv_zigzag_shard result (same Hq, Hkv, weights) on every rank.  out_local /
+    lse_local: the rank's KV group (Z x g x L x d, Z x g x L) with only its zigzag chunks written.
+    Ranks own differently sized chunks when groups have different rank counts, so every rank
+    broadcasts its two chunks (exact sizes) and each lands at (its group's heads, its chunks'
+    rows) of the full Z x Hq layout."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    if world <= Hkv and (weights is None or world < Hkv):
+        return gather_heads(out_local, lse_local, Hq, Hkv, group, out, lse)
+    rank = dist.get_rank(group)
+    g = Hq // Hkv
+    Z, _, L = out_local.shape[:3]
+    M = -(-L // block)
+    spec = []  # per rank: (kv group, [(row lo, row hi) of its two chunks])
+    for r in range(world):
+        sh, rows = kv_zigzag_shard(Hq, Hkv, world, r, weights)
+        if rows is None:
+            spec.append((sh.kv_lo, [(0, L), (L, L)]))
+            continue
+        _, sub, n = rows
+        c = -(-M // (2 * n)) * block
+        spec.append((sh.kv_lo, [(min(L, ch * c), min(L, (ch + 1) * c))
+                                for ch in (sub, 2 * n - 1 - sub)]))
+    if out is None:
+        out = torch.empty((Z, Hq) + tuple(out_local.shape[2:]), dtype=out_local.dtype,
+                          device=out_local.device)
+    if lse is None:
+        lse = torch.empty((Z, Hq, L), dtype=lse_local.dtype, device=lse_local.device)
+    for x, dst in ((out_local, out), (lse_local, lse)):
+        tail = tuple(x.shape[3:])
+        for r, (kv, chunks) in enumerate(spec):  # one broadcast per rank, exact sizes
+            n_rows = sum(b - a for a, b in chunks)
+            if r == rank:
+                buf = torch.cat([x[:, :, a:b] for a, b in chunks], dim=2).contiguous()
+            else:
+                buf = torch.empty((Z, g, n_rows) + tail, dtype=x.dtype, device=x.device)
+            _broadcast(buf, r, group)
+            o = 0
+            for a, b in chunks:
+                dst[:, kv * g:(kv + 1) * g, a:b] = buf[:, :, o:o + b - a]
+                o += b - a
+    return out, lse
+
+
+def _broadcast(t: torch.Tensor, src: int, group=None) -> None:
+    """In-place broadcast; over gloo, device tensors are staged through host memory."""
+    import torch.distributed as dist
+    if dist.get_backend(group) == "gloo" and t.is_cuda:
+        h = t.cpu()
+        dist.broadcast(h, dist.get_global_rank(group, src) if group else src, group=group)
+        t.copy_(h)
+    else:
+        dist.broadcast(t, dist.get_global_rank(group, src) if group else src, group=group)

@@ -62,6 +62,19 @@ def _worker(rank, world, port, part, shape, ret):
             rs.append(r)
         g.wait()
         r = rs[0]
+    elif part in ("kv_zigzag", "kv_weighted"):
+        # one KV head per rank, a group's ranks split by zigzag rows; kv_weighted: ranks per group
+        # by the layer plan's visits per group (3 ranks over 2 groups: 2 + 1)
+        w = None
+        if part == "kv_weighted":
+            cnt = fp.discover_select(q, k, cfg)[0].counts.sum(dim=(0, 1)).double()
+            g = Hq // Hkv
+            w = [float(cnt[i * g:(i + 1) * g].sum()) for i in range(Hkv)]
+        s, rows = shard.kv_zigzag_shard(Hq, Hkv, world, rank, w)
+        r = fp.PrefillRunner(*shard.local_slices(q, k, v, s), cfg, rows=rows).capture()
+        r.replay_discover()
+        r.replay_attend()
+        out, lse = shard.gather_kv_zigzag(r.out, r.lse, Hq, Hkv, 128, weights=w)
     else:
         rows = shard.row_shard(world, rank) if part == "rows" else shard.zigzag_shard(world, rank)
         r = fp.PrefillRunner(q, k, v, cfg, rows=rows).capture()
@@ -84,6 +97,8 @@ def _worker(rank, world, port, part, shape, ret):
     ("kv_chunked", 4, (12, 2, 1000)),  # 3 Q heads per rank: chunks of 2 + 1, ragged L
     ("rows", 2, (8, 2, 3000)),   # interleaved query blocks, ragged last block
     ("zigzag", 3, (8, 2, 3000)),
+    ("kv_zigzag", 4, (8, 2, 3000)),  # 2 ranks per KV group, each with the group's 4 Q heads
+    ("kv_weighted", 3, (8, 2, 3000)),  # ranks per KV group by plan visits (2 + 1)
 ])
 def test_sharded_layer_gathers_bit_identical(fp, part, world, shape):
     Hq, Hkv, L = shape
@@ -99,8 +114,9 @@ def test_sharded_layer_gathers_bit_identical(fp, part, world, shape):
     assert torch.equal(ret["lse"], r.lse.cpu()), part
 
 
-@pytest.mark.parametrize("part,chunks", [("kv", 2), ("kv", 1), ("rows", 1)])
-def test_bench_two_ranks_shared_gpu(fp, part, chunks):
+@pytest.mark.parametrize("part,chunks,extra", [("kv", 2, []), ("kv", 1, []), ("rows", 1, []),
+                                               ("kv_zigzag", 1, ["--hq", "16", "--hkv", "1"])])
+def test_bench_two_ranks_shared_gpu(fp, part, chunks, extra):
     """bench.py --gpus 2 under torchrun (shared-GPU gloo mode): one strong-scaling JSON line with
     per-rank times and the gather inside the step (kv: chunked P2P gather overlapped with the
     next chunk's compute, or one all-gather after all kernels)."""
@@ -108,7 +124,7 @@ def test_bench_two_ranks_shared_gpu(fp, part, chunks):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
            "--gpus", "2", "--steps", "3", "--warmup", "3", "--L", "8192", "--no-e2e",
-           "--partition", part, "--gather-chunks", str(chunks)]
+           "--partition", part, "--gather-chunks", str(chunks)] + extra
     res = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-3000:]
     lines = [x for x in res.stdout.splitlines() if x.startswith("{")]

@@ -177,3 +177,74 @@ def test_head_chunks():
     assert head_chunks(3, 2) == [(0, 2), (2, 3)]
     assert head_chunks(1, 4) == [(0, 1)]
     assert head_chunks(16, 3) == [(0, 6), (6, 11), (11, 16)]
+
+
+def _kvz_worker(rank, world, port, Hkv, out, lse, ret, weights=None):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_06199_b200.shard import gather_kv_zigzag, kv_zigzag_shard, zigzag_blocks
+    Hq, L = out.shape[1], out.shape[2]
+    s, rows = kv_zigzag_shard(Hq, Hkv, world, rank, weights)
+    own = torch.zeros(L, dtype=torch.bool)
+    blocks = range(-(-L // 128)) if rows is None else zigzag_blocks(-(-L // 128), rows[2], rows[1])
+    for I in blocks:
+        own[I * 128:(I + 1) * 128] = True
+    # the rank's KV group; rows it does not own are garbage (fpb_*_zigzag leaves them unwritten)
+    o = out[:, s.q_lo:s.q_hi].clone()
+    l_ = lse[:, s.q_lo:s.q_hi].clone()
+    o[:, :, ~own] = float("nan")
+    l_[:, :, ~own] = -7.0
+    go, gl = gather_kv_zigzag(o, l_, Hq, Hkv, 128, weights=weights)
+    ret[rank] = bool(torch.equal(go, out) and torch.equal(gl, lse))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,Hq,Hkv,L,weights", [
+    (2, 4, 1, 1000, None), (4, 8, 2, 1300, None), (4, 4, 4, 700, None), (3, 6, 1, 2000, None),
+    (8, 16, 4, 1500, (20.1, 10.9, 6.2, 16.3)),  # ranks per group 3, 2, 1, 2
+    (4, 8, 4, 900, (1.0, 1.0, 1.0, 1.0))])      # weighted, one rank per group
+def test_kv_zigzag_gather(world, Hq, Hkv, L, weights):
+    """kv_zigzag partition: one KV group per rank (or per world/Hkv ranks, each with all of the
+    group's Q heads and its zigzag chunks); the gather reassembles the full layer on every rank,
+    ragged last block included."""
+    g = torch.Generator().manual_seed(world * 31 + L)
+    out = torch.randn((1, Hq, L, 128), generator=g)
+    lse = torch.randn((1, Hq, L), generator=g)
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_kvz_worker, args=(world, _free_port(), Hkv, out, lse, ret, weights), nprocs=world,
+             join=True)
+    assert all(ret[r] for r in range(world)), dict(ret)
+
+
+@pytest.mark.parametrize("world,Hq,Hkv,weights", [
+    (1, 8, 2, None), (2, 8, 2, None), (4, 8, 2, None), (8, 32, 4, None), (3, 6, 1, None),
+    (8, 32, 4, (20.1, 10.9, 6.2, 16.3)), (7, 32, 4, (1, 5, 1, 1)), (4, 8, 4, (3, 1, 2, 2))])
+def test_kv_zigzag_shard_covers_layer(world, Hq, Hkv, weights):
+    """Every (Q head, query block) is owned by exactly one rank; a rank holds one KV head's group
+    (or whole groups when world <= Hkv)."""
+    from paper_2603_06199_b200.shard import kv_zigzag_shard, zigzag_blocks
+    M = 37
+    seen = {}
+    for r in range(world):
+        s, rows = kv_zigzag_shard(Hq, Hkv, world, r, weights)
+        assert s.q_hi - s.q_lo == (s.kv_hi - s.kv_lo) * (Hq // Hkv)
+        blocks = range(M) if rows is None else zigzag_blocks(M, rows[2], rows[1])
+        for h in range(s.q_lo, s.q_hi):
+            for I in blocks:
+                assert (h, I) not in seen
+                seen[(h, I)] = r
+    assert len(seen) == Hq * M
+
+
+def test_kv_group_ranks_by_weight():
+    """Heavier KV groups get more ranks; every group at least one; equal split without weights."""
+    from paper_2603_06199_b200.shard import kv_group_ranks
+    assert kv_group_ranks(4, 8) == [2, 2, 2, 2]
+    assert kv_group_ranks(4, 8, [20.1, 10.9, 6.2, 16.3]) == [3, 2, 1, 2]
+    assert kv_group_ranks(4, 4, [9, 1, 1, 1]) == [1, 1, 1, 1]
+    assert sum(kv_group_ranks(8, 13, list(range(1, 9)))) == 13
+    with pytest.raises(ValueError):
+        kv_group_ranks(4, 6)  # equal split needs divisibility

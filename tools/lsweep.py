@@ -102,6 +102,10 @@ def markdown(path):
           "per box)\n")
     print("Step = max over ranks (no data-path collective). `kv_group`: the north_star partition "
           "(rank owns KV heads; Qwen3 at 8 ranks splits each group's 8 Q heads 4+4).")
+    print("`kv_zigzag`: one KV head per rank as in kv_group, but the G/Hkv ranks of a group "
+          "each take all of its Q heads and split the query blocks in zigzag chunks (G = 8 only; "
+          "identical to kv_group for G <= Hkv). `kv_weighted`: the same with ranks per KV group "
+          "by the layer plan's visits per group (`shard.kv_group_ranks`).")
     print("`rows`: rank r owns query blocks r, r+G, ... of every head (`fpb_*_rows`), K/V "
           "replicated. `zigzag`: rank r owns contiguous chunks r and 2G-1-r of 2G chunks "
           "(`fpb_*_zigzag`), K/V replicated. The O+LSE all-gather after the kernels is not timed "
@@ -127,6 +131,8 @@ def main():
     ap.add_argument("--alpha", type=float, default=0.12)
     ap.add_argument("--out", default="")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--Gs", default="2,4,8")
+    ap.add_argument("--parts", default="kv_group,kv_zigzag,kv_weighted,rows,zigzag")
     args = ap.parse_args()
     hbm, tc = peaks()
     out = open(args.out, "a") if args.out else None
@@ -157,11 +163,22 @@ def main():
         if out:
             out.write(line + "\n")
             out.flush()
-        for G in (2, 4, 8):
-            for part in ("kv_group", "rows", "zigzag"):
+        # per-KV-group block visits of the whole layer (the kv_weighted partition's calibration)
+        cnt = fp.discover_select(q, k, cfg)[0].counts.sum(dim=(0, 1)).double()
+        gq = HQ // HKV
+        kvw = [float(cnt[i * gq:(i + 1) * gq].sum()) for i in range(HKV)]
+        for G in (int(x) for x in args.Gs.split(",")):
+            for part in args.parts.split(","):
+                if part in ("kv_zigzag", "kv_weighted") and G <= HKV:
+                    continue  # identical to kv_group
                 per_rank = []
                 for rank in range(G):
-                    if part == "kv_group":
+                    if part in ("kv_zigzag", "kv_weighted"):
+                        s, rows = shard.kv_zigzag_shard(HQ, HKV, G, rank,
+                                                        kvw if part == "kv_weighted" else None)
+                        ql, kl, vl = (x.contiguous() for x in shard.local_slices(q, k, v, s))
+                        td, ta, _, vis = stage(ql, kl, vl, cfg, grid, tau, reps, rows=rows)
+                    elif part == "kv_group":
                         s = shard.kv_group_shard(HQ, HKV, G, rank)
                         ql, kl, vl = (x.contiguous() for x in shard.local_slices(q, k, v, s))
                         td, ta, _, vis = stage(ql, kl, vl, cfg, grid, tau, reps)

@@ -402,6 +402,29 @@ def time_runner(runner, stream, flush, reps, gather=None, dist=None):
     return ts
 
 
+def discovery_tensor_view(args, M, ms_disc, pk):
+    """The discovery stage against the tensor pipe, its binding resource at <= 128K (the HBM view
+    above is what north_star asks for).  Executed MMA FLOPs: per (z, h, query block I) one UMMA
+    per 128-block chunk of key blocks J <= I, two of them (k̄ hi and lo, 128 x 128 x 128 each), an
+    M = 64 UMMA (half) for a last chunk with <= 64 causal key blocks (csrc/discover.cu).
+    Algorithmic FLOPs: 2 d per (query row, causal key block) — the block-approximate logits once."""
+    full = half = 0
+    for I in range(M):
+        n = I // B + 1
+        if I % B < 64:
+            full += n - 1
+            half += 1
+        else:
+            full += n
+    per_head_mma = 2 * (full + 0.5 * half) * 2.0 * B * B * D
+    executed = per_head_mma * args.hq / (ms_disc * 1e-3) / 1e12
+    algorithmic = args.hq * B * (M * (M + 1) / 2) * 2.0 * D / (ms_disc * 1e-3) / 1e12
+    return {"executed_tflops": executed, "frac_of_burst": executed / pk["tc_burst"],
+            "algorithmic_tflops": algorithmic,
+            "note": "stage time (pooling + discovery + select) in the denominator; executed = "
+                    "split-precision UMMAs incl. chunk padding, 2.5x the algorithmic logits"}
+
+
 def kernel_launches(runner, fallback: int) -> int:
     """Kernel nodes in the runner's two CUDA graphs (what one step launches)."""
     try:
@@ -641,7 +664,9 @@ def run_gpu_arm(args, rank, world, dist):
                                "achieved": disc_bytes / (ms_disc * 1e-3) / 1e9,
                                "peak": pk["hbm"], "unit": "GB/s",
                                "frac": disc_bytes / (ms_disc * 1e-3) / 1e9 / pk["hbm"],
-                               "bytes": disc_bytes} if world == 1 else None,
+                               "bytes": disc_bytes,
+                               "tensor": discovery_tensor_view(args, M, ms_disc, pk)}
+        if world == 1 else None,
         "clocks": clocks.summary(),
         "gpu_launches": launches * args.steps,
         "gpu_launches_per_step": launches,

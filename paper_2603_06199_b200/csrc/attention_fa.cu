@@ -38,6 +38,12 @@ constexpr int kRing = 5;                      // shared K/V tile ring
 #define FPB_SCHED_SLEEP 256  // ns; measured: 128K -5.7%, 32K / 256K neutral (r1_ab_fa_sched_sleep)
 #endif
 constexpr float kRescaleThreshold = 8.0f;     // lazy O rescale (log2 units)
+// P is handed to the PV MMA in kPParts column parts (keys 128 / kPParts each), one mbarrier each
+#ifndef FPB_FA_PPARTS
+#define FPB_FA_PPARTS 2
+#endif
+constexpr int kPParts = FPB_FA_PPARTS;
+static_assert(kPParts == 1 || kPParts == 2 || kPParts == 4, "P parts");
 constexpr int kPartFloats = kBlock * kHeadDim + 2 * kBlock;  // one row's partial: O, m, l
 constexpr double kPhaseBytes = 64.0 * 1024 * 1024;  // K/V bytes of one KV-range phase (L2 budget)
 // Timing probes (wrong numerics; tools/ab_probe.sh): 1 = softmax without max/exp2 (P = raw S),
@@ -111,7 +117,7 @@ struct FaSmem {
   uint8_t ring[kRing][kTile];
   uint64_t q_full[2], q_empty[2];
   uint64_t kv_full[kRing], kv_empty[kRing];
-  uint64_t s_full[2], p_half[2], p_full[2], o_done[2], o_free[2];
+  uint64_t s_full[2], p_part[2][kPParts], o_done[2], o_free[2];
   uint64_t meta_full[2][2], meta_empty[2][2];
   SlotMeta meta[2][2];
   uint32_t tmem_base;
@@ -182,8 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&s.q_full[i]), 1);
       mbar_init(smem_u32(&s.q_empty[i]), 1);
       mbar_init(smem_u32(&s.s_full[i]), 1);
-      mbar_init(smem_u32(&s.p_half[i]), 4);
-      mbar_init(smem_u32(&s.p_full[i]), 4);
+      for (int k = 0; k < kPParts; ++k) mbar_init(smem_u32(&s.p_part[i][k]), 4);
       mbar_init(smem_u32(&s.o_done[i]), 1);
       mbar_init(smem_u32(&s.o_free[i]), 4);
       for (int p = 0; p < 2; ++p) {
@@ -421,15 +426,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           // SW128 descriptors are linear in the address field (addr >> 4, 14 bits; SMEM < 256 KiB),
           // so every K step is the tile's base descriptor plus a constant
           const uint64_t vdesc = sdesc_sw128(smem_u32(s.ring[r]), kTile / 2, 1024);
-          // keys 0..63 as soon as the first half of P is in TMEM, keys 64..127 after the rest
-          for (int half = 0; half < 2; ++half) {
-            mbar_wait(smem_u32(half ? &s.p_full[sl] : &s.p_half[sl]), (S.bc - 1) & 1);
+          // each part of the keys as soon as that part of P is in TMEM
+          for (int part = 0; part < kPParts; ++part) {
+            mbar_wait(smem_u32(&s.p_part[sl][part]), (S.bc - 1) & 1);
             tc_fence_after();
-            TR_ADD(9 + half);  // MMA: waiting for P half
+            TR_ADD(part + 1 == kPParts ? 10 : 9);  // MMA: waiting for a P part
             if (leader && FPB_FA_PROBE != 3 && FPB_FA_PROBE != 4 && FPB_FA_PROBE < 6) {
 #pragma unroll
-              for (int k4 = 0; k4 < 4; ++k4) {
-                const int ks = half * 4 + k4;
+              for (int k4 = 0; k4 < 8 / kPParts; ++k4) {
+                const int ks = part * (8 / kPParts) + k4;
                 mma_bf16_ts(o_tmem, s_tmem + ks * 8, vdesc + (uint64_t)(ks * 2048 >> 4), idesc_pv,
                             (m > 0 || ks > 0 || S.cont) ? 1u : 0u);
               }
@@ -547,12 +552,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           return fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3));
         };
-        // P = exp2(S * to_bits - m) for columns [64 half, 64 half + 64), packed in place:
+        // P = exp2(S * to_bits - m) for the columns of one part, packed in place:
         // v[c/2] <- bf16x2(p_c, p_c+1); row sums in 8 independent accumulators
+        constexpr int kPC = kBlock / kPParts;  // columns per part
         auto exp_half = [&](int half, float neg_m) {
           if (full) {
 #pragma unroll
-            for (int c = half * 64; c < half * 64 + 64; c += 2) {
+            for (int c = half * kPC; c < half * kPC + kPC; c += 2) {
               // MUFU ex2 for every element: FMA-pipe emulation measured slower on B200
               // (profiles/r1_fa_trace.txt)
               float x0, x1;
@@ -564,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           } else {
 #pragma unroll
-            for (int c = half * 64; c < half * 64 + 64; c += 2) {
+            for (int c = half * kPC; c < half * kPC + kPC; c += 2) {
               const float p0 = FA_EX2(fmaf(__uint_as_float(v[c]), sc, neg_m));
               const float p1 = FA_EX2(fmaf(__uint_as_float(v[c + 1]), sc, neg_m));
               const int a = ((c >> 1) & 3) * 2;
@@ -621,16 +627,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         }
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
+        for (int half = 0; half < kPParts; ++half) {
 #if FPB_FA_PROBE != 1 && FPB_FA_PROBE != 4 && FPB_FA_PROBE < 6
-          if (half == 1) exp_half(1, -m_used);
+          if (half > 0) exp_half(half, -m_used);
 #endif
-          tmem_st32(s_addr + half * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[half * 32]));
+          // P of this part's keys -> TMEM columns (kPC / 2) half .. (bf16 pairs over S)
+          if constexpr (kPParts == 1) {
+            tmem_st32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+            tmem_st32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+          } else if constexpr (kPParts == 2)
+            tmem_st32(s_addr + half * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[half * 32]));
+          else
+            tmem_st16(s_addr + half * 16, *reinterpret_cast<uint32_t(*)[16]>(&v[half * 16]));
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(half ? &s.p_full[sl] : &s.p_half[sl]));
-          TR_ADD(3 + half);  // softmax: exp + pack + TMEM store, per half
+          if (lane == 0) mbar_arrive(smem_u32(&s.p_part[sl][half]));
+          TR_ADD(half + 1 == kPParts ? 4 : 3);  // softmax: exp + pack + TMEM store, per part
         }
         l += ((bs[0] + bs[1]) + (bs[2] + bs[3])) + ((bs[4] + bs[5]) + (bs[6] + bs[7]));
       }

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -140,6 +141,15 @@ int restrict_zigzag(Dims* D, int32_t rank, int32_t world) {
 // The tcgen05/TMA kernels cover the tile shape d = B = 128; every other shape the reference
 // accepts runs the SIMT kernels of generic.cu.
 bool tc_path(const Dims& D) { return D.d == kHeadDim && D.B == kBlock; }
+
+// The tcgen05 path moves Q / K / V / O with TMA tensor maps, bulk copies and 16-byte vector
+// accesses: their base addresses must be 16-byte aligned (a misaligned view would fault).
+int check_align16(std::initializer_list<const void*> ptrs) {
+  for (const void* q : ptrs)
+    if (reinterpret_cast<uintptr_t>(q) & 15u)
+      return fail(FPB_EVALIDATION, "tensor base address %p is not 16-byte aligned", q);
+  return FPB_OK;
+}
 
 int check_dtype(fpb_dtype t) {
   return (t == FPB_F32 || t == FPB_BF16) ? FPB_OK : fail(FPB_EUSAGE, "bad dtype %d", (int)t);
@@ -292,6 +302,7 @@ int fpb_pool_keys(const fpb_problem* p, fpb_dtype dtype, const void* K, float* p
   int rc = resolve(p, &D);
   if (rc || (rc = check_dtype(dtype))) return rc;
   if (!K || !pooled) return fail(FPB_EUSAGE, "null pointer");
+  if (tc_path(D) && (rc = check_align16({K}))) return rc;
   if (tc_path(D))
     FPB_CUDA(launch_pool_keys(D, dtype == FPB_BF16, K, pooled, nullptr, S(stream)));
   else
@@ -311,6 +322,7 @@ int fpb_approx_block_scores(const fpb_problem* p, fpb_dtype dtype, const void* Q
     return FPB_OK;
   }
   if ((rc = need_ws(workspace_bytes, ws_discover(D, dtype), workspace))) return rc;
+  if ((rc = check_align16({Q}))) return rc;
   const DiscWs w = disc_ws(D, workspace, dtype);
   FPB_CUDA(launch_split_pooled(D, pooled, w.kbar, S(stream)));
   const __nv_bfloat16* qp = static_cast<const __nv_bfloat16*>(Q);
@@ -375,6 +387,7 @@ static int discover_select_rows(const fpb_problem* p, int32_t row_begin, int32_t
     return FPB_OK;
   }
   if (D.Mr == 0) return FPB_OK;  // this row shard owns no query block
+  if ((rc = check_align16({Q, K}))) return rc;
   const DiscWs w = disc_ws(D, workspace, dtype);
   const __nv_bfloat16* qp;
   if ((rc = discover_prepare(D, dtype, Q, K, nullptr, w, S(stream), &qp))) return rc;
@@ -563,6 +576,7 @@ static int attention_common(const fpb_problem* p, fpb_dtype dtype, const void* Q
                                 static_cast<float*>(workspace), S(stream)));
     return FPB_OK;
   }
+  if ((rc = check_align16({Q, K, V, out}))) return rc;
   const __nv_bfloat16 *q = static_cast<const __nv_bfloat16*>(Q),
                       *k = static_cast<const __nv_bfloat16*>(K),
                       *v = static_cast<const __nv_bfloat16*>(V);

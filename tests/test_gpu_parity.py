@@ -535,3 +535,31 @@ def test_qwen3_32k_plan_invariants_and_full_plan_identity(fp):
     st = fp.AttentionStats()
     fp.block_sparse_attention(q, k, v, plan, grid, tau, st)
     assert st.block_visits == int(counts.sum())
+
+
+def test_misaligned_views_rejected(fp):
+    """The tcgen05 path moves Q / K / V / O with TMA and bulk copies: a tensor whose base address
+    is not 16-byte aligned (a 2-byte-offset view) is a ValidationError, not a device fault."""
+    L = 1024
+    q, k, v = (x.cuda() for x in fp.workload.composite(3, 1, 2, 1, L))
+    cfg = fp.PipelineConfig()
+
+    def shifted(t):  # same shape, base address + 2 bytes
+        flat = torch.empty(t.numel() + 8, dtype=t.dtype, device=t.device)
+        view = flat[1:1 + t.numel()].view(t.shape)
+        view.copy_(t)
+        return view
+
+    with pytest.raises(fp.ValidationError):
+        fp.discover_select(shifted(q), k, cfg)
+    with pytest.raises(fp.ValidationError):
+        fp.discover_select(q, shifted(k), cfg)
+    plan = fp.discover_select(q, k, cfg)[0]
+    grid = fp.make_block_grid(L, 128)
+    with pytest.raises(fp.ValidationError):
+        fp.block_sparse_attention(q, k, shifted(v), plan, grid, cfg.resolved_scale(128))
+    with pytest.raises(fp.ValidationError):
+        fp.pool_keys(shifted(k), grid)
+    torch.cuda.synchronize()  # the context is still healthy
+    res = fp.block_sparse_attention(q, k, v, plan, grid, cfg.resolved_scale(128))
+    assert torch.isfinite(res.lse).all()

@@ -20,6 +20,8 @@
  *   - fpb_* functions take DEVICE pointers and are stream-ordered on `stream` (cudaStream_t passed
  *     as void*; NULL = legacy default stream).  They never allocate on the hot path: scratch comes
  *     from a caller-provided workspace sized by fpb_workspace_bytes().
+ *   - With d = B = 128 (the tcgen05 path) Q, K, V and out must be 16-byte aligned (TMA / bulk
+ *     copies); a misaligned base address returns 2 (validation) instead of faulting.
  *   - fpb_host_* functions take HOST pointers, copy in, run, copy out and synchronise; they are what
  *     the C++ drop-in layer (include/fpb200/bsattn.hpp) calls.
  *   - Return codes mirror the reference CLI's exit codes (bsattn_main.cpp:671-692):

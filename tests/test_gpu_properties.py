@@ -6,7 +6,9 @@ fp32 output so the properties are not hidden by output rounding).
     within the bf16 bars: P is rounded to bf16 against an order-dependent running max);
   * monotone LSE: adding blocks to a row never lowers its log-sum-exp;
   * convex hull: every output channel lies within the [min, max] of V over the attended keys;
-  * 20 random shapes (L, Hq, Hkv incl. GQA and ragged L): full causal plan == dense within 1e-4.
+  * 20 random shapes (L, Hq, Hkv incl. GQA and ragged L): full causal plan == dense within 1e-4;
+  * discovery KATs (test_discovery.cpp:70-134): identical query rows, energy bound, sentinels;
+  * selection: alpha-monotone plans, alpha = 0 keeps every causal block (test_selection.cpp).
 """
 import numpy as np
 import pytest
@@ -133,3 +135,64 @@ def test_acceptance_full_plan_equals_dense(fp, port, L, Hq, Hkv):
                                   out_dtype=torch.float32)
     b = fp.dense_attention(_cuda(q), _cuda(k), _cuda(v), tau, out_dtype=torch.float32)
     assert err(_np(a.out), _np(b.out))[0] <= 1e-4 and err(_np(a.lse), _np(b.lse))[0] <= 1e-4
+
+
+def test_discovery_identical_rows_kat(fp, port):
+    """test_discovery.cpp:70-89: when every query row of a block is the same vector q, each
+    causal pair's local max is the scaled logit q . k̄_J and its energy is the row count (all
+    exp2 terms are 1); the ragged last block counts its real rows only."""
+    L, d = 300, 128
+    rng = np.random.default_rng(1)
+    qrow = bf16_round(rng.normal(size=(d,)).astype(np.float32))
+    q = np.broadcast_to(qrow, (1, 1, L, d)).copy()
+    k = bf16_round(rng.normal(size=(1, 1, L, d)).astype(np.float32))
+    tau = float(port.scale(d))
+    m = fp.discover(_cuda(q), _cuda(k), fp.make_block_grid(L, 128), tau)
+    en, lm = _np(m.energy)[0, 0], _np(m.local_max)[0, 0]
+    pooled = port.pool_keys(k, 128)[0, 0]
+    M = -(-L // 128)
+    for I in range(M):
+        rows = min(128, L - I * 128)
+        for J in range(I + 1):
+            want = float(np.dot(qrow.astype(np.float64), pooled[J].astype(np.float64))) * \
+                tau * 1.4426950408889634
+            assert abs(lm[I, J] - want) <= 1e-4 * max(1.0, abs(want))
+            assert abs(en[I, J] - rows) <= 1e-3 * rows
+
+
+def test_discovery_energy_bound_and_sentinels(fp, port):
+    """test_discovery.cpp:91-134: 0 < S_IJ <= rows of block I for causal pairs; J > I holds the
+    sentinels (energy 0, local max FLT_LOWEST, score 0); each score row sums to ~1."""
+    L = 1500
+    q, k, _ = _layer(51, 2, 1, L)
+    tau = float(port.scale(128))
+    m = fp.discover(_cuda(q), _cuda(k), fp.make_block_grid(L, 128), tau)
+    en, lm, sc = _np(m.energy), _np(m.local_max), _np(m.score)
+    M = en.shape[2]
+    tri = np.tril(np.ones((M, M), bool))
+    rows = np.array([min(128, L - I * 128) for I in range(M)], np.float32)[:, None]
+    for h in range(2):
+        e = en[0, h]
+        assert np.all(e[tri] > 0) and np.all((e <= rows * (1 + 1e-6))[tri])
+        assert np.all(e[~tri] == 0) and np.all(sc[0, h][~tri] == 0)
+        assert np.all(lm[0, h][~tri] == np.finfo(np.float32).min)
+        assert np.allclose(sc[0, h].sum(axis=1), 1.0, atol=1e-5)
+
+
+def test_selection_alpha_monotone(fp):
+    """test_selection.cpp:58-120: a larger alpha never activates a block a smaller one drops
+    (plans nest), and alpha = 0 keeps every causal block."""
+    L = 4096
+    q, k, _ = _layer(53, 4, 2, L)
+    M = L // 128
+    prev = None
+    for alpha in (0.0, 0.05, 0.12, 0.3, 1.0):
+        _, _, gm = fp.discover_select(_cuda(q), _cuda(k), fp.PipelineConfig(alpha=alpha),
+                                      want_mask=True)
+        mask = _np(gm.active).astype(bool)
+        if alpha == 0.0:
+            tri = np.tril(np.ones((M, M), bool))[None, :, :, None]
+            assert np.array_equal(mask, np.broadcast_to(tri, mask.shape))
+        if prev is not None:
+            assert not np.any(mask & ~prev)
+        prev = mask

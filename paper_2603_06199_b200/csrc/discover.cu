@@ -560,6 +560,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---- outputs: energy / local_max rows (thread-owned J), then normalisation
       const size_t map_row = (((size_t)z * D.Hq + h) * D.M + I) * (size_t)N;
       if (prm.out.energy || prm.out.local_max) {
+        // an M = 64 last chunk wrote its m / S entries through another thread-to-J mapping
+        if (FPB_DISC_M64) named_bar_sync(ebar, kEpiThreads);
         for (int J = et; J < N; J += kEpiThreads) {
           if (prm.out.energy) prm.out.energy[map_row + J] = (J <= I) ? S_s[J] : 0.f;
           if (prm.out.local_max) prm.out.local_max[map_row + J] = (J <= I) ? m_s[J] : kNegSentinel;
@@ -641,6 +643,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             prm.out.counts[((size_t)z * D.M + I) * D.Hq + h] = base;
         }
       }
+      // the next item's M = 64 last chunk writes m_s / S_s entries that other threads of this
+      // warpgroup read in the tail above: nobody starts it before everyone is done (racecheck)
+      if (FPB_DISC_M64) named_bar_sync(ebar, kEpiThreads);
       DT_ADD(4);  // epilogue: fill + counts
     }
   }

@@ -377,3 +377,51 @@ def _broadcast(t: torch.Tensor, src: int, group=None) -> None:
         t.copy_(h)
     else:
         dist.broadcast(t, dist.get_global_rank(group, src) if group else src, group=group)
+
+
+def prefill_sharded(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, config, partition: str = "kv",
+                    group=None, weights=None, out_dtype: torch.dtype | None = None):
+    """One layer's FlashPrefill step split over the ranks of `group` (one process per GPU), the
+    full O / LSE assembled on every rank.  Every rank passes the whole layer (Z x Hq x L x d Q,
+    Z x Hkv x L x d K / V, on its own device); it computes only its share:
+
+      "kv"        kv_group_shard  — KV-head groups, a group's Q heads split (north_star)
+      "kv_zigzag" kv_zigzag_shard — KV-head groups, a group's query blocks split (zigzag); with
+                  `weights` (work per KV group, e.g. a calibration plan's visits) heavier groups
+                  get more ranks
+      "rows" / "zigzag" — every head's query blocks interleaved / in zigzag chunks
+
+    Returns (out, lse).  Bit-identical to the unsharded call: every (z, h, query block) is
+    computed independently (discovery.hpp:87-88, selection.hpp:71-72, attention.hpp:59-60)."""
+    import torch.distributed as dist
+    from . import bsattn as fp
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    Z, Hq, L, d = q.shape
+    Hkv = k.shape[1]
+    grid = fp.make_block_grid(L, config.block_size)
+    tau = config.resolved_scale(d)
+
+    def run(ql, kl, vl, rows):
+        plan, _, _ = fp.discover_select(ql, kl, config, rows=rows)
+        return fp.block_sparse_attention(ql, kl, vl, plan, grid, tau, out_dtype=out_dtype,
+                                         rows=rows)
+
+    if world == 1:
+        res = run(q, k, v, None)
+        return res.out, res.lse
+    if partition == "kv":
+        s = kv_group_shard(Hq, Hkv, world, rank)
+        res = run(*local_slices(q, k, v, s), None)
+        return gather_heads(res.out, res.lse, Hq, Hkv, group)
+    if partition == "kv_zigzag":
+        s, rows = kv_zigzag_shard(Hq, Hkv, world, rank, weights)
+        res = run(*local_slices(q, k, v, s), rows)
+        return gather_kv_zigzag(res.out, res.lse, Hq, Hkv, config.block_size, group,
+                                weights=weights)
+    if partition == "rows":
+        res = run(q, k, v, row_shard(world, rank))
+        return gather_rows(res.out, res.lse, config.block_size, group)
+    if partition == "zigzag":
+        res = run(q, k, v, zigzag_shard(world, rank))
+        return gather_zigzag(res.out, res.lse, config.block_size, group)
+    raise ValueError(f"unknown partition {partition!r}")

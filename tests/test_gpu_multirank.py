@@ -62,6 +62,9 @@ def _worker(rank, world, port, part, shape, ret):
             rs.append(r)
         g.wait()
         r = rs[0]
+    elif part.startswith("api_"):  # the one-call API: shard.prefill_sharded
+        out, lse = shard.prefill_sharded(q, k, v, cfg, partition=part[4:])
+        r = None
     elif part in ("kv_zigzag", "kv_weighted"):
         # one KV head per rank, a group's ranks split by zigzag rows; kv_weighted: ranks per group
         # by the layer plan's visits per group (3 ranks over 2 groups: 2 + 1)
@@ -82,7 +85,8 @@ def _worker(rank, world, port, part, shape, ret):
         r.replay_attend()
         g = shard.gather_rows if part == "rows" else shard.gather_zigzag
         out, lse = g(r.out, r.lse, 128)
-    r.check()
+    if r is not None:
+        r.check()
     if rank == 0:
         ret["out"] = out.cpu()
         ret["lse"] = lse.cpu()
@@ -99,6 +103,9 @@ def _worker(rank, world, port, part, shape, ret):
     ("zigzag", 3, (8, 2, 3000)),
     ("kv_zigzag", 4, (8, 2, 3000)),  # 2 ranks per KV group, each with the group's 4 Q heads
     ("kv_weighted", 3, (8, 2, 3000)),  # ranks per KV group by plan visits (2 + 1)
+    ("api_kv", 2, (8, 2, 2048)),       # shard.prefill_sharded, each partition
+    ("api_kv_zigzag", 4, (8, 2, 2500)),
+    ("api_zigzag", 3, (4, 2, 1700)),
 ])
 def test_sharded_layer_gathers_bit_identical(fp, part, world, shape):
     Hq, Hkv, L = shape

@@ -563,3 +563,32 @@ def test_misaligned_views_rejected(fp):
     torch.cuda.synchronize()  # the context is still healthy
     res = fp.block_sparse_attention(q, k, v, plan, grid, cfg.resolved_scale(128))
     assert torch.isfinite(res.lse).all()
+
+
+def test_prefill_host_concurrent_threads(fp):
+    """fpb_host_prefill keeps a per-thread device arena and streams: two host threads calling it at
+    once (ctypes releases the GIL) get the same results as sequential calls."""
+    import threading
+    L = 3000
+    ins = [fp.workload.composite(61 + i, 1, 4, 2, L) for i in range(2)]
+    cfg = fp.PipelineConfig()
+
+    def run(i, res):
+        q, k, v = (x.pin_memory() for x in ins[i])
+        out = torch.empty(q.shape, dtype=torch.bfloat16).pin_memory()
+        lse = torch.empty(q.shape[:3], dtype=torch.float32).pin_memory()
+        for _ in range(3):
+            fp.prefill_host(q, k, v, cfg, out, lse)
+        res[i] = (out.clone(), lse.clone())
+
+    seq = {}
+    for i in range(2):
+        run(i, seq)
+    par = {}
+    ts = [threading.Thread(target=run, args=(i, par)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i in range(2):
+        assert torch.equal(par[i][0], seq[i][0]) and torch.equal(par[i][1], seq[i][1])

@@ -39,6 +39,9 @@ constexpr int kRing = 5;                      // shared K/V tile ring
 #endif
 constexpr float kRescaleThreshold = 8.0f;     // lazy O rescale (log2 units)
 // P is handed to the PV MMA in kPParts column parts (keys 128 / kPParts each), one mbarrier each
+#ifndef FPB_FA_TMEM0
+#define FPB_FA_TMEM0 1  // measured: 32K -0.6%, 128K -2.5% (profiles/r2_ab_tmem0.jsonl)
+#endif
 #ifndef FPB_FA_PPARTS
 #define FPB_FA_PPARTS 2
 #endif
@@ -206,7 +209,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+#if FPB_FA_TMEM0
+  // all 512 columns of the SM's TMEM are allocated, so the allocation starts at lane 0, column 0:
+  // a compile-time base keeps the TMEM addresses out of the control warps' (spilled) registers
+  constexpr uint32_t tmem = 0;
+  if (threadIdx.x == 0 && s.tmem_base != 0u) __trap();
+#else
   const uint32_t tmem = s.tmem_base;
+#endif
   // 384 threads x 168 regs at launch; hand the control warpgroup's share to the softmax WGs
   // (128 x 72 + 256 x 216 = 64512 = the launch allocation: any more and setmaxnreg.inc blocks)
   if (warp < 4) {

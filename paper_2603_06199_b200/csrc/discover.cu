@@ -61,6 +61,9 @@ constexpr uint32_t kEpiBar = 1;               // named barriers 1, 2: the two ep
 #define FPB_DISC_PRODUCER_WARP 2
 #endif
 constexpr uint32_t kMmaWarp = FPB_DISC_MMA_WARP;
+#ifndef FPB_DISC_TMEM0
+#define FPB_DISC_TMEM0 0
+#endif
 #ifndef FPB_DISC_M64
 #define FPB_DISC_M64 1
 #endif
@@ -193,7 +196,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+#if FPB_DISC_TMEM0
+  // the whole TMEM (512 columns) is allocated, so the allocation starts at lane 0, column 0
+  constexpr uint32_t tmem = 0;
+  if (threadIdx.x == 0 && s.tmem_base != 0u) __trap();
+#else
   const uint32_t tmem = s.tmem_base;
+#endif
   const int nck = (D.M + kBlock - 1) / kBlock;
 
   if constexpr (NQ == 1) {
